@@ -1,0 +1,193 @@
+/*
+ * ipm.h — C ABI of libipm.so, the B200-native (sm_100a) data-parallel hot path of the
+ * GPU interior point method of arxiv 2405.03584 (Liu, Fredriksson, Markidis).
+ *
+ * The library solves the convex QP (eq:qp, bounds split out as in P:176)
+ *
+ *     min 1/2 x^T H x + g^T x    s.t.   l <= A x <= u ,   xl <= x <= xu
+ *
+ * with Algorithm 1: every search direction is a Jacobi-preconditioned CG
+ * solve of the condensed Newton system
+ *
+ *     K dx = rhs ,   K = H + Sigma_b + A^T Sigma_c A                                  (1)
+ *
+ * which is the Schur complement of the reduced system eq:2x2_reduced:
+ * Sigma_b = S_lx^-1 Lam_lx + S_ux^-1 Lam_ux (the diagonal part of Q) and
+ * Sigma_c = Lam_lA S_lA^-1 + Lam_uA S_uA^-1 (B^T D^-1 B with B = [A_l; -A_u]).
+ *
+ * Conventions (all calls):
+ *   - Values fp64 (IEEE binary64), CSR row offsets int64, CSR column indices int32.
+ *   - Every pointer argument is DEVICE memory on the context's device unless the
+ *     parameter name ends in _host.  Vectors are dense, unit stride.
+ *   - Absent bounds are +-INFINITY.  Bound families are masked full-length vectors:
+ *     entry i of an m-vector belongs to row i of A, entry j of an n-vector to x_j.
+ *     Entries of slack/multiplier vectors whose bound is absent are 0.
+ *   - All work is stream-ordered on the cudaStream_t given to ipm_create.  Calls that
+ *     return host values (stats, traces, objective) synchronise that stream.
+ *   - No call throws across the ABI; every failure returns a status and sets a
+ *     message readable with ipm_last_error(ctx) (or ipm_last_error(NULL) when no
+ *     context exists yet).
+ *   - Results are bitwise reproducible run to run on the same device and shapes: no
+ *     floating-point atomics, fixed-order reductions, stored A^T.
+ */
+#ifndef IPM_B200_IPM_H
+#define IPM_B200_IPM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IPM_ABI_VERSION 1
+
+typedef struct ipm_ctx ipm_ctx;
+typedef void *ipm_stream_t; /* a cudaStream_t / CUstream (NULL = legacy default stream) */
+
+typedef enum {
+    IPM_OK = 0,
+    IPM_NOT_CONVERGED = 1,     /* iteration limit N reached; last iterate retrievable */
+    IPM_ERR_INVALID = 2,       /* bad dims, CSR not sorted/unique/in range, l>=u, xl>=xu, NaN data */
+    IPM_ERR_PCG_BREAKDOWN = 3, /* p^T K p <= 0 or non-finite inside PCG: loss of SPD */
+    IPM_ERR_NONFINITE = 4,     /* non-finite residual / step; last finite iterate kept */
+    IPM_ERR_CUDA = 5,          /* a CUDA runtime error (message has the CUDA error string) */
+    IPM_ERR_OOM = 6,           /* workspace smaller than ipm_workspace_size() */
+    IPM_ERR_NCCL = 7,          /* NCCL failure in the row-sharded path */
+    IPM_ERR_STATE = 8          /* call not valid in this state (e.g. solution before solve) */
+} ipm_status;
+
+/* Options.  Fill with ipm_options_default() and then override fields. */
+typedef struct {
+    int32_t size;               /* = sizeof(ipm_options); ABI versioning */
+    double mu_tol;              /* 1e-8   Alg. 1 line 11 mu_tol (reading R6) */
+    double mu0_scale;           /* 0.1    mu0 = mu0_scale * sum(lam s) / #bounds (R5) */
+    double mu_divisor;          /* 10     Alg. 1 line 14 "mu <- mu/10" */
+    double tau;                 /* 0.995  fraction to the boundary (R6) */
+    int32_t max_ipm_iter;       /* 100    Alg. 1 "for i <- 1 to N" */
+    int32_t pcg_schedule;       /* 0: rtol = max(floor, min(rtol_max, factor*mu))  (D6)
+                                   1: SPEC S:238 rtol = max(1e-10, min(1e-2, 0.1 mu)) */
+    double pcg_rtol_max;        /* 1e-6 */
+    double pcg_rtol_mu_factor;  /* 1e-3 */
+    double pcg_rtol_floor;      /* 1e-12 */
+    double pcg_atol;            /* 1e-13  absolute floor on ||r||_2 */
+    int32_t pcg_max_iter;       /* 0 => 10*n */
+    int32_t predictor_corrector;/* 0: Alg. 1 verbatim (default); 1: Mehrotra (R18, option) */
+    int32_t trace;              /* 1: record one ipm_trace_rec per IPM iteration */
+    int32_t use_graph;          /* 1: PCG loop as a CUDA graph with a device-side WHILE node */
+    double warm_shift;          /* 1e-3   theta of the warm-start rule (R15) */
+} ipm_options;
+
+/* Problem description for ipm_create.  Large arrays are BORROWED (the caller keeps them
+ * alive and unchanged until ipm_destroy); small ones are copied at create. */
+typedef struct {
+    int64_t n;                  /* variables, >= 1 */
+    int64_t m;                  /* rows of A, >= 0 */
+    int64_t nnz;                /* nonzeros of A, >= 0 */
+    const double *H;            /* BORROWED. Row-major SPD Hessian; element (i,j) at H[i*ldh + j].
+                                   Sharded (nranks>1): only rows [row_begin,row_end), i.e. H points
+                                   at the local block, element (i,j) at H[(i-row_begin)*ldh + j].
+                                   Written only by ipm_update_hessian_rank2. */
+    int64_t ldh;                /* >= n.  ldh even and H 16-byte aligned enable 128-bit loads. */
+    const double *g;            /* n, copied */
+    const int64_t *A_rowptr;    /* m+1, BORROWED; A_rowptr[0]=0, A_rowptr[m]=nnz, non-decreasing */
+    const int32_t *A_col;       /* nnz, BORROWED; strictly increasing within each row, in [0,n) */
+    const double *A_val;        /* nnz, BORROWED; finite */
+    const double *l, *u;        /* m each, copied; -INF / +INF = absent; l < u where both finite */
+    const double *xl, *xu;      /* n each, copied; xl < xu where both finite */
+    int64_t row_begin, row_end; /* row block of H (and of all x-space vectors) owned by this rank */
+    int32_t rank, nranks;       /* nranks == 1 => unsharded (row_begin=0,row_end=n) */
+    const void *nccl_unique_id_host; /* HOST pointer to an ncclUniqueId (128 bytes), nranks > 1 */
+} ipm_problem;
+
+typedef struct {
+    int32_t status;             /* final ipm_status of the last ipm_solve */
+    int32_t ipm_iters;
+    int64_t pcg_iters_total;
+    int32_t pcg_iters_max;
+    int32_t pcg_stalls;         /* PCG solves that hit pcg_max_iter without reaching rtol */
+    int32_t pcg_restarts;       /* true-residual restarts */
+    double mu_final;
+    double kkt_inf;             /* ||r||_inf over the nine residual families (R4) */
+    double obj;                 /* 1/2 x^T H x + g^T x at the returned iterate */
+    double t_solve_ms;          /* device time of the last ipm_solve (CUDA events) */
+    double t_pcg_ms;            /* device time spent inside PCG solves */
+} ipm_stats;
+
+typedef struct {
+    int32_t it;
+    int32_t pcg_iters;
+    double mu;
+    double kkt_inf;
+    double alpha_x, alpha_lam;
+    double pcg_relres;          /* final true relative residual of the PCG solve */
+    double obj;
+} ipm_trace_rec;
+
+/* Fill defaults (documented per field above). */
+void ipm_options_default(ipm_options *opt);
+
+/* Bytes of device workspace ipm_create needs for this problem (host-only arithmetic). */
+ipm_status ipm_workspace_size(const ipm_problem *prob, const ipm_options *opt, size_t *bytes);
+
+/* Create a context: validates the problem (host copies of the O(n+m+nnz) data; H is checked
+ * for non-finite entries on the device), copies g and the bounds, builds the stored
+ * transpose A^T on the device (deterministic counting sort), caches diag(H).
+ * workspace: device buffer of >= ipm_workspace_size() bytes, 256-byte aligned, owned by the
+ * caller, not touched by anyone else until ipm_destroy.  The context's device is the
+ * current CUDA device at the time of the call. */
+ipm_status ipm_create(ipm_ctx **ctx, const ipm_problem *prob, const ipm_options *opt,
+                      void *workspace, size_t workspace_bytes, ipm_stream_t stream);
+
+/* Run Algorithm 1 to convergence (IPM_OK), to the iteration limit (IPM_NOT_CONVERGED) or
+ * to an error.  Cold start from the S:290 initial point unless ipm_set_iterate /
+ * ipm_warm_start was called since the last solve. */
+ipm_status ipm_solve(ipm_ctx *ctx);
+
+/* Copy the current iterate out (device pointers; NULL = skip).  obj_host: host double. */
+ipm_status ipm_get_solution(ipm_ctx *ctx, double *x, double *lam_lA, double *lam_uA,
+                            double *lam_lx, double *lam_ux, double *obj_host);
+
+ipm_status ipm_get_stats(ipm_ctx *ctx, ipm_stats *stats);
+/* Copy up to cap trace records of the last solve (requires opt.trace = 1). */
+ipm_status ipm_get_trace(ipm_ctx *ctx, ipm_trace_rec *recs_host, int32_t cap, int32_t *count_host);
+
+/* C4 (SQP sequence): replace g (device, n); modify the borrowed H in place:
+ * H <- H + alpha u u^T + beta v v^T (u, v device n-vectors, full length even when sharded);
+ * diag(H) cache is updated; then ipm_warm_start makes the next solve start from the
+ * current solution by the R15 rule. */
+ipm_status ipm_set_linear_term(ipm_ctx *ctx, const double *g);
+ipm_status ipm_update_hessian_rank2(ipm_ctx *ctx, const double *u, double alpha,
+                                    const double *v, double beta);
+ipm_status ipm_warm_start(ipm_ctx *ctx);
+
+/* Replace / read the iterate (masked full-length layout; order lA, uA, lx, ux). */
+ipm_status ipm_set_iterate(ipm_ctx *ctx, const double *x, const double *const s4[4],
+                           const double *const lam4[4], double mu);
+ipm_status ipm_get_iterate(ipm_ctx *ctx, double *x, double *const s4[4], double *const lam4[4],
+                           double *mu_host);
+
+/* Test hooks — one stage of the hot path on caller-supplied diagonals (device):
+ *   ipm_op_apply: y = K v with K of (1), Sigma_b = sig_b (n), Sigma_c = sig_c (m)
+ *   ipm_op_diag : d = diag(K) = diag(H) + sig_b + colsq(A, sig_c)
+ *   ipm_pcg     : Jacobi-PCG on K x = rhs from x = 0 to ||r|| <= rtol ||rhs|| (true residual
+ *                 confirmed); iters_host gets the iteration count. */
+ipm_status ipm_op_apply(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *v,
+                        double *y);
+ipm_status ipm_op_diag(ipm_ctx *ctx, const double *sig_b, const double *sig_c, double *d);
+ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *rhs,
+                   double *x, double rtol, int32_t *iters_host);
+
+/* Number of kernel launches the library issued since create (graph nodes count once per
+ * executed node); used by bench.py's gpu_launches. */
+int64_t ipm_kernel_launches(const ipm_ctx *ctx);
+
+/* Context-local message of the last failure (or the last create failure for NULL). */
+const char *ipm_last_error(const ipm_ctx *ctx);
+void ipm_destroy(ipm_ctx *ctx);
+int32_t ipm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IPM_B200_IPM_H */

@@ -1,0 +1,116 @@
+// common.cuh — shared device helpers of libipm.so (sm_100a).
+//
+// Determinism contract ("bitwise reproducible"): every floating-point
+// reduction below has a fixed association order that depends only on the launch shape
+// (grid/block size, which are functions of the problem dimensions), never on timing:
+// lane-strided partial sums -> xor-shuffle tree -> per-warp slots in shared memory summed
+// in warp order -> per-block partials summed in block order by the last block to finish.
+// No floating-point atomics anywhere.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ipm {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Sum over a group of G consecutive lanes (G power of two <= 32); all lanes get the result.
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum; result valid in ALL threads.  `sh` needs blockDim/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += sh[i];  // fixed order, every thread
+    return t;
+}
+
+__device__ __forceinline__ double block_min(double v, double *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_min(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = sh[0];
+    for (int i = 1; i < nw; ++i) t = fmin(t, sh[i]);
+    return t;
+}
+
+__device__ __forceinline__ double block_max(double v, double *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = sh[0];
+    for (int i = 1; i < nw; ++i) t = fmax(t, sh[i]);
+    return t;
+}
+
+// "Last block done" election (threadfence-reduction pattern).  Every block calls it after
+// writing its partials; exactly one block (the last to arrive) gets true and must reset the
+// counter.  The reduction order over partials is then fixed (block order), so which block
+// happens to be last does not change the bits.
+__device__ __forceinline__ bool last_block(unsigned int *counter) {
+    __shared__ bool am_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int prev = atomicAdd(counter, 1u);
+        am_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (am_last) __threadfence();
+    return am_last;
+}
+
+// Fixed-order sum of `cnt` partials by one block (all threads get it).
+__device__ __forceinline__ double sum_partials(const double *part, int cnt, double *sh) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) v += ((volatile const double *)part)[i];
+    return block_sum(v, sh);
+}
+
+__device__ __forceinline__ double min_partials(const double *part, int cnt, double *sh) {
+    double v = INFINITY;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) v = fmin(v, ((volatile const double *)part)[i]);
+    return block_min(v, sh);
+}
+
+__device__ __forceinline__ double max_partials(const double *part, int cnt, double *sh) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) v = fmax(v, ((volatile const double *)part)[i]);
+    return block_max(v, sh);
+}
+
+__device__ __forceinline__ bool finite_d(double v) { return fabs(v) <= 1.7976931348623157e308; }
+
+}  // namespace ipm

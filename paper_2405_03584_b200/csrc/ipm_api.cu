@@ -1,0 +1,817 @@
+// ipm_api.cu — host side of libipm.so: the C ABI of include/ipm.h.
+//
+// Algorithm 1 runs as a host loop over device kernels; ALL vectors
+// stay resident on the device (the paper moves residuals, D and the solution across PCIe
+// every iteration, P:232-238 — here only ~20 scalars come back per IPM iteration for the
+// mu logic of Alg. 1 lines 10-15).  The PCG inner loop (line 2) is a CUDA graph whose
+// conditional WHILE node is re-armed by the device, so a whole PCG solve is one launch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ipm.h"
+#include "kernels.h"
+#include "state.h"
+
+#define IPM_EXPORT extern "C" __attribute__((visibility("default")))
+
+using namespace ipm;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Layout {
+    size_t total = 0;
+    size_t take(size_t bytes) {
+        const size_t off = total;
+        total += (bytes + 255) & ~size_t(255);
+        return off;
+    }
+};
+
+struct Offsets {
+    size_t sc;
+    size_t nvec[40];
+    size_t mvec[40];
+    size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad;
+    int n_nvec, n_mvec;
+    int nchunk;
+};
+
+constexpr int kNVec = 30;   // n-space vectors in Vecs (see assign_vectors)
+constexpr int kMVec = 24;   // m-space vectors
+
+Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, Layout &L) {
+    Offsets o{};
+    o.sc = L.take(sizeof(Scalars));
+    for (int i = 0; i < kNVec; ++i) o.nvec[i] = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+    for (int i = 0; i < kMVec; ++i) o.mvec[i] = L.take(sizeof(double) * std::max<int64_t>(m, 1));
+    o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) * gemv_ncb((int)ncols));
+    o.part = L.take(sizeof(double) * kMaxPartials * 8);
+    o.ATrp = L.take(sizeof(int64_t) * (nloc + 1));
+    o.ATcol = L.take(sizeof(int) * std::max<int64_t>(nnz_loc, 1));
+    o.ATval = L.take(sizeof(double) * std::max<int64_t>(nnz_loc, 1));
+    o.g = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+    o.xl = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+    o.xu = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+    o.l = L.take(sizeof(double) * std::max<int64_t>(m, 1));
+    o.u = L.take(sizeof(double) * std::max<int64_t>(m, 1));
+    o.diagH = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+    o.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(128, m));
+    o.cnt = L.take(sizeof(int) * (size_t)o.nchunk * std::max<int64_t>(nloc, 1));
+    o.bad = L.take(sizeof(unsigned long long));
+    return o;
+}
+
+}  // namespace
+
+struct ipm_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;   // user stream
+    cudaStream_t cap = nullptr;  // private capture stream
+    ipm_options opt{};
+    int64_t n = 0, m = 0, nnz = 0;
+    int row0 = 0, nloc = 0, rank = 0, nranks = 1;
+    char *ws = nullptr;
+    Prob P{};
+    Vecs V{};
+    Scalars *sc = nullptr;
+    Scalars *hsc = nullptr;  // pinned host copy
+    int G = 8;
+    int ncb = 1;
+    int gemv_grid = 148;
+    int64_t nbounds = 0;
+    // graph
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraphConditionalHandle handle = 0;
+    bool graph_ready = false;
+    // state
+    bool have_iterate = false;   // V holds a valid iterate (after a solve or set_iterate)
+    bool user_iterate = false;   // set_iterate called: next solve starts from it
+    bool warm_pending = false;   // ipm_warm_start called
+    double mu = 0.0;
+    ipm_stats stats{};
+    std::vector<ipm_trace_rec> trace;
+    std::string err;
+    int64_t launches = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+ipm_status fail(ipm_ctx *c, ipm_status s, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    else g_create_error = buf;
+    return s;
+}
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) return fail(ctx, IPM_ERR_CUDA, "%s: %s (%s:%d)", #call,              \
+                                           cudaGetErrorString(e_), __FILE__, __LINE__);            \
+    } while (0)
+
+#define CKL()                                                                                       \
+    do {                                                                                            \
+        cudaError_t e_ = cudaGetLastError();                                                        \
+        if (e_ != cudaSuccess) return fail(ctx, IPM_ERR_CUDA, "kernel launch: %s (%s:%d)",         \
+                                           cudaGetErrorString(e_), __FILE__, __LINE__);            \
+    } while (0)
+
+#define TRY(expr)                          \
+    do {                                   \
+        ipm_status s_ = (expr);            \
+        if (s_ != IPM_OK) return s_;       \
+    } while (0)
+
+ipm_status sync_scalars(ipm_ctx *ctx) {
+    CKL();
+    CK(cudaMemcpyAsync(ctx->hsc, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return IPM_OK;
+}
+
+void assign_vectors(ipm_ctx *c, const Offsets &o) {
+    char *b = c->ws;
+    double *nv[kNVec];
+    double *mv[kMVec];
+    for (int i = 0; i < kNVec; ++i) nv[i] = reinterpret_cast<double *>(b + o.nvec[i]);
+    for (int i = 0; i < kMVec; ++i) mv[i] = reinterpret_cast<double *>(b + o.mvec[i]);
+    Vecs &V = c->V;
+    int k = 0;
+    V.x = nv[k++]; V.s_lx = nv[k++]; V.s_ux = nv[k++]; V.lam_lx = nv[k++]; V.lam_ux = nv[k++];
+    V.rH = nv[k++]; V.r_lx = nv[k++]; V.r_ux = nv[k++]; V.rc_lx = nv[k++]; V.rc_ux = nv[k++]; V.Hx = nv[k++];
+    V.sig_b = nv[k++]; V.Minv = nv[k++]; V.rhs = nv[k++]; V.dx = nv[k++];
+    V.ds_lx = nv[k++]; V.ds_ux = nv[k++]; V.dl_lx = nv[k++]; V.dl_ux = nv[k++];
+    V.ads_lx = nv[k++]; V.ads_ux = nv[k++]; V.adl_lx = nv[k++]; V.adl_ux = nv[k++];
+    V.pr = nv[k++]; V.pz = nv[k++]; V.pp = nv[k++]; V.py = nv[k++];
+    int j = 0;
+    V.s_lA = mv[j++]; V.s_uA = mv[j++]; V.lam_lA = mv[j++]; V.lam_uA = mv[j++];
+    V.r_lA = mv[j++]; V.r_uA = mv[j++]; V.rc_lA = mv[j++]; V.rc_uA = mv[j++]; V.Ax = mv[j++];
+    V.sig_c = mv[j++]; V.r2_l = mv[j++]; V.r2_u = mv[j++]; V.w = mv[j++]; V.Adx = mv[j++];
+    V.ds_lA = mv[j++]; V.ds_uA = mv[j++]; V.dl_lA = mv[j++]; V.dl_uA = mv[j++];
+    V.ads_lA = mv[j++]; V.ads_uA = mv[j++]; V.adl_lA = mv[j++]; V.adl_uA = mv[j++];
+    V.lamd = mv[j++]; V.pt = mv[j++];
+    V.ypart = reinterpret_cast<double *>(b + o.ypart);
+    for (int i = 0; i < 8; ++i) V.part[i] = reinterpret_cast<double *>(b + o.part) + (size_t)i * kMaxPartials;
+}
+
+int choose_group(int64_t nnz_loc, int64_t nloc, int ncb) {
+    const double avg = nloc > 0 ? (double)nnz_loc / (double)nloc : 0.0;
+    const double work = std::max(avg, (double)ncb);
+    if (work <= 6) return 4;
+    if (work <= 12) return 8;
+    if (work <= 24) return 16;
+    return 32;
+}
+
+double pcg_rtol(const ipm_options &o, double mu) {
+    if (o.pcg_schedule == 1) return std::max(1e-10, std::min(1e-2, 0.1 * mu));
+    return std::max(o.pcg_rtol_floor, std::min(o.pcg_rtol_max, o.pcg_rtol_mu_factor * mu));
+}
+
+// ---------------------------------------------------------------------------- operators
+// y = K v with the current sig_b/sig_c (t and ypart are scratch).  mode 1: r = rhs - K v.
+ipm_status op_apply(ipm_ctx *ctx, const double *v, double *out, const double *rhs, int mode) {
+    const Prob &P = ctx->P;
+    const Vecs &V = ctx->V;
+    launch_spmv(P, v, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 0, ctx->st);
+    launch_gemv(P, v, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+    launch_apply_reduce(P, ctx->G, ctx->ncb, V.ypart, V.sig_b, v, V.pt, out, rhs, V.part[5], ctx->sc, mode, ctx->st);
+    ctx->launches += (P.m > 0 ? 1 : 0) + 2;
+    CKL();
+    return IPM_OK;
+}
+
+ipm_status build_graph(ipm_ctx *ctx) {
+    if (ctx->graph_ready) return IPM_OK;
+    CK(cudaGraphCreate(&ctx->graph, 0));
+    CK(cudaGraphConditionalHandleCreate(&ctx->handle, ctx->graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = ctx->handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, ctx->graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(ctx->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle, 1, ctx->cap);
+    cudaGraph_t captured = nullptr;
+    CK(cudaStreamEndCapture(ctx->cap, &captured));
+    CK(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
+    ctx->graph_ready = true;
+    return IPM_OK;
+}
+
+struct PcgOut {
+    int64_t iters = 0;
+    double relres = 0.0;
+    bool stalled = false;
+    int restarts = 0;
+};
+
+// Solve K dx = rhs (V.rhs -> V.dx) with the current diagonals; Minv already set.
+ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
+    const Prob &P = ctx->P;
+    Vecs &V = ctx->V;
+    int64_t maxit = ctx->opt.pcg_max_iter > 0 ? ctx->opt.pcg_max_iter : 10 * (int64_t)ctx->n;
+    launch_pcg_init(P, V, ctx->sc, V.rhs, V.dx, rtol, ctx->opt.pcg_atol, maxit, ctx->st);
+    ctx->launches += 1;
+    CKL();
+    if (ctx->opt.use_graph) TRY(build_graph(ctx));
+    out = PcgOut{};
+    int64_t it_prev = 0;
+    for (int round = 0;; ++round) {
+        if (ctx->opt.use_graph) {
+            CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+            TRY(sync_scalars(ctx));
+        } else {
+            // host-driven fallback: batches of 16 iterations with device-side early exit
+            for (;;) {
+                for (int b = 0; b < 16; ++b)
+                    launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st);
+                TRY(sync_scalars(ctx));
+                ctx->launches += 16 * (3 + (P.m > 0 ? 1 : 0));
+                if (ctx->hsc->done) break;
+            }
+        }
+        const Scalars &h = *ctx->hsc;
+        if (ctx->opt.use_graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * (3 + (P.m > 0 ? 1 : 0));
+        it_prev = h.it;
+        if (h.breakdown) {
+            out.iters = h.it;
+            return fail(ctx, IPM_ERR_PCG_BREAKDOWN, "PCG breakdown at iteration %lld (p^T K p = %g)",
+                        (long long)h.it, h.pKp);
+        }
+        // true residual confirmation: r = rhs - K dx
+        TRY(op_apply(ctx, V.dx, V.pr, V.rhs, 1));
+        TRY(sync_scalars(ctx));
+        const double res2 = ctx->hsc->res2, tol2 = ctx->hsc->tol2, rhs2 = ctx->hsc->rhs2;
+        out.iters = ctx->hsc->it;
+        out.relres = rhs2 > 0 ? std::sqrt(res2 / rhs2) : 0.0;
+        if (!std::isfinite(res2)) return fail(ctx, IPM_ERR_NONFINITE, "non-finite PCG residual");
+        if (res2 <= tol2) break;
+        if (ctx->hsc->it >= maxit || round >= 8) {
+            out.stalled = true;
+            break;
+        }
+        out.restarts++;
+        launch_pcg_restart(P, V, ctx->sc, ctx->st);
+        ctx->launches += 1;
+        CKL();
+    }
+    return IPM_OK;
+}
+
+// Hx (GEMV tiles) + Ax (SpMV), then the residual kernels at the given mu.
+ipm_status residuals(ipm_ctx *ctx, double mu) {
+    const Prob &P = ctx->P;
+    const Vecs &V = ctx->V;
+    launch_gemv(P, V.x, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+    launch_spmv(P, V.x, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
+    launch_residuals(P, V, ctx->G, ctx->sc, mu, ctx->st);
+    ctx->launches += 2 + 2 * (P.m > 0 ? 1 : 0);
+    CKL();
+    return IPM_OK;
+}
+
+double kkt_inf(const Scalars &h) { return std::max(h.rH_max, std::max(h.prim_max, h.comp_max)); }
+
+// One Newton direction (Alg. 1 lines 2-3) into V.dx / V.d* ; step lengths in sc->alpha_*.
+ipm_status direction(ipm_ctx *ctx, double mu, int mode, double smu, double tau, int aff, PcgOut &po, float &tpcg) {
+    const Prob &P = ctx->P;
+    const Vecs &V = ctx->V;
+    launch_rhs(P, V, ctx->G, mu, mode, smu, ctx->st);
+    ctx->launches += 1 + (P.m > 0 ? 1 : 0);
+    CKL();
+    CK(cudaEventRecord(ctx->ev[2], ctx->st));
+    TRY(pcg_solve(ctx, pcg_rtol(ctx->opt, mu), po));
+    CK(cudaEventRecord(ctx->ev[3], ctx->st));
+    float ms = 0.f;
+    CK(cudaEventSynchronize(ctx->ev[3]));
+    CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+    tpcg += ms;
+    launch_spmv(P, V.dx, nullptr, V.Adx, nullptr, ctx->sc, 0, 0, ctx->st);
+    launch_recover(P, V, ctx->sc, tau, aff, ctx->st);
+    ctx->launches += 1 + 2 * (P.m > 0 ? 1 : 0);
+    CKL();
+    return IPM_OK;
+}
+
+ipm_status start_point(ipm_ctx *ctx) {
+    const Prob &P = ctx->P;
+    const Vecs &V = ctx->V;
+    if (ctx->user_iterate) {
+        ctx->user_iterate = false;
+        return IPM_OK;
+    }
+    const int warm = ctx->warm_pending ? 1 : 0;
+    ctx->warm_pending = false;
+    launch_init_x(P, V, warm, ctx->opt.warm_shift, ctx->st);
+    launch_spmv(P, V.x, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
+    launch_init_slacks(P, V, ctx->sc, warm, ctx->opt.warm_shift, ctx->st);
+    ctx->launches += 2 + 2 * (P.m > 0 ? 1 : 0);
+    TRY(sync_scalars(ctx));
+    if (ctx->nbounds == 0) ctx->mu = ctx->opt.mu_tol;                                   // R13
+    else ctx->mu = ctx->opt.mu0_scale * ctx->hsc->sum_ls / (double)ctx->nbounds;      // R5
+    return IPM_OK;
+}
+
+ipm_status solve_impl(ipm_ctx *ctx) {
+    const ipm_options &o = ctx->opt;
+    ctx->trace.clear();
+    ipm_stats &S = ctx->stats;
+    S = ipm_stats{};
+    CK(cudaMemsetAsync(&ctx->sc->nonfinite, 0, sizeof(int64_t), ctx->st));
+    CK(cudaEventRecord(ctx->ev[0], ctx->st));
+    TRY(start_point(ctx));
+    ctx->have_iterate = true;
+    TRY(residuals(ctx, ctx->mu));
+    TRY(sync_scalars(ctx));
+    double mu = ctx->mu;
+    float tpcg = 0.f;
+    ipm_status status = IPM_NOT_CONVERGED;
+    const bool pc = o.predictor_corrector && ctx->nbounds > 0;
+    int k = 0;
+    for (k = 1; k <= o.max_ipm_iter; ++k) {
+        launch_sigma(ctx->P, ctx->V, ctx->G, ctx->st);
+        ctx->launches += 1 + (ctx->P.m > 0 ? 1 : 0);
+        PcgOut po, po2;
+        if (!pc) {
+            TRY(direction(ctx, mu, 0, 0.0, o.tau, 0, po, tpcg));
+        } else {
+            // Mehrotra (R18): affine direction, sigma = (mu_aff/mu_cur)^3, corrector
+            launch_sum_ls(ctx->P, ctx->V, ctx->sc, ctx->st);
+            TRY(direction(ctx, mu, 1, 0.0, 1.0, 1, po, tpcg));
+            launch_muaff(ctx->P, ctx->V, ctx->sc, ctx->st);
+            ctx->launches += 2 * (1 + (ctx->P.m > 0 ? 1 : 0));
+            TRY(sync_scalars(ctx));
+            const double nb = (double)ctx->nbounds;
+            const double mu_cur = ctx->hsc->sum_ls / nb;
+            const double mu_aff = ctx->hsc->muaff / nb;
+            const double r = mu_aff / mu_cur;
+            const double smu = r * r * r * mu_cur;
+            TRY(direction(ctx, mu, 2, smu, o.tau, 0, po2, tpcg));
+        }
+        launch_update(ctx->P, ctx->V, ctx->sc, ctx->st);
+        ctx->launches += 1 + (ctx->P.m > 0 ? 1 : 0);
+        if (pc) {
+            launch_sum_ls(ctx->P, ctx->V, ctx->sc, ctx->st);
+            ctx->launches += 1 + (ctx->P.m > 0 ? 1 : 0);
+        }
+        TRY(residuals(ctx, pc ? 0.0 : mu));
+        TRY(sync_scalars(ctx));
+        const Scalars &h = *ctx->hsc;
+        const int64_t its = po.iters + po2.iters;
+        S.pcg_iters_total += its;
+        S.pcg_iters_max = std::max<int32_t>(S.pcg_iters_max, (int32_t)std::max(po.iters, po2.iters));
+        S.pcg_stalls += (po.stalled ? 1 : 0) + (po2.stalled ? 1 : 0);
+        S.pcg_restarts += po.restarts + po2.restarts;
+        if (h.nonfinite) {
+            status = fail(ctx, IPM_ERR_NONFINITE, "non-finite residual or step at IPM iteration %d", k);
+            break;
+        }
+        double nrm;
+        if (pc) {
+            mu = h.sum_ls / (double)ctx->nbounds;
+            nrm = std::max(h.rH_max, std::max(h.prim_max, h.ls_max));
+        } else {
+            nrm = kkt_inf(h);
+        }
+        if (o.trace) {
+            ipm_trace_rec r{};
+            r.it = k;
+            r.pcg_iters = (int32_t)its;
+            r.mu = mu;
+            r.kkt_inf = nrm;
+            r.alpha_x = h.alpha_x;
+            r.alpha_lam = h.alpha_l;
+            r.pcg_relres = std::max(po.relres, po2.relres);
+            r.obj = h.obj;
+            ctx->trace.push_back(r);
+        }
+        if (pc) {
+            if (nrm < o.mu_tol) {
+                status = IPM_OK;
+                break;
+            }
+            continue;
+        }
+        if (nrm < mu) {                                  // Alg. 1 lines 10-15
+            if (mu <= o.mu_tol) {
+                status = IPM_OK;
+                break;
+            }
+            mu = mu / o.mu_divisor;
+        }
+    }
+    ctx->mu = mu;
+    // final residuals at the final mu (r_c with the current mu) for reporting
+    TRY(residuals(ctx, mu));
+    TRY(sync_scalars(ctx));
+    CK(cudaEventRecord(ctx->ev[1], ctx->st));
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+    S.status = status;
+    S.ipm_iters = std::min(k, o.max_ipm_iter);
+    S.mu_final = mu;
+    S.kkt_inf = kkt_inf(*ctx->hsc);
+    S.obj = ctx->hsc->obj;
+    S.t_solve_ms = ms;
+    S.t_pcg_ms = tpcg;
+    return status;
+}
+
+ipm_status validate_host(ipm_ctx *ctx, const ipm_problem *p, std::vector<int64_t> &rp, std::vector<int> &col) {
+    const int64_t n = p->n, m = p->m, nnz = p->nnz;
+    if (rp.size() != (size_t)(m + 1)) return fail(ctx, IPM_ERR_INVALID, "rowptr size");
+    if (rp[0] != 0 || rp[m] != nnz) return fail(ctx, IPM_ERR_INVALID, "A_rowptr[0] must be 0 and A_rowptr[m] == nnz");
+    for (int64_t i = 0; i < m; ++i) {
+        if (rp[i + 1] < rp[i]) return fail(ctx, IPM_ERR_INVALID, "A_rowptr decreasing at row %lld", (long long)i);
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            if (col[k] < 0 || col[k] >= n)
+                return fail(ctx, IPM_ERR_INVALID, "A_col out of range in row %lld", (long long)i);
+            if (k > rp[i] && col[k] <= col[k - 1])
+                return fail(ctx, IPM_ERR_INVALID, "A_col not strictly increasing (unsorted or duplicate) in row %lld",
+                            (long long)i);
+        }
+    }
+    return IPM_OK;
+}
+
+ipm_status check_bounds(ipm_ctx *ctx, const std::vector<double> &lo, const std::vector<double> &hi, const char *what) {
+    for (size_t i = 0; i < lo.size(); ++i) {
+        if (std::isnan(lo[i]) || std::isnan(hi[i])) return fail(ctx, IPM_ERR_INVALID, "%s bound %zu is NaN", what, i);
+        if (lo[i] == INFINITY || hi[i] == -INFINITY)
+            return fail(ctx, IPM_ERR_INVALID, "%s bound %zu: lower=+inf or upper=-inf", what, i);
+        if (std::isfinite(lo[i]) && std::isfinite(hi[i]) && !(lo[i] < hi[i]))
+            return fail(ctx, IPM_ERR_INVALID, "%s bounds %zu: need lower < upper (equal bounds are rejected, R10)",
+                        what, i);
+    }
+    return IPM_OK;
+}
+
+}  // namespace
+
+// ================================================================================= C ABI
+IPM_EXPORT int32_t ipm_abi_version(void) { return IPM_ABI_VERSION; }
+
+IPM_EXPORT void ipm_options_default(ipm_options *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->size = (int32_t)sizeof(ipm_options);
+    o->mu_tol = 1e-8;
+    o->mu0_scale = 0.1;
+    o->mu_divisor = 10.0;
+    o->tau = 0.995;
+    o->max_ipm_iter = 100;
+    o->pcg_schedule = 0;
+    o->pcg_rtol_max = 1e-6;
+    o->pcg_rtol_mu_factor = 1e-3;
+    o->pcg_rtol_floor = 1e-12;
+    o->pcg_atol = 1e-13;
+    o->pcg_max_iter = 0;
+    o->predictor_corrector = 0;
+    o->trace = 0;
+    o->use_graph = 1;
+    o->warm_shift = 1e-3;
+}
+
+static void local_rows(const ipm_problem *p, int64_t &row0, int64_t &nloc) {
+    if (p->nranks > 1) {
+        row0 = p->row_begin;
+        nloc = p->row_end - p->row_begin;
+    } else {
+        row0 = 0;
+        nloc = p->n;
+    }
+}
+
+IPM_EXPORT ipm_status ipm_workspace_size(const ipm_problem *p, const ipm_options *opt, size_t *bytes) {
+    (void)opt;
+    if (!p || !bytes) return fail(nullptr, IPM_ERR_INVALID, "null argument");
+    if (p->n < 1 || p->m < 0 || p->nnz < 0) return fail(nullptr, IPM_ERR_INVALID, "bad dimensions");
+    int64_t row0, nloc;
+    local_rows(p, row0, nloc);
+    Layout L;
+    plan(nloc, p->n, p->m, p->nnz, L);   // nnz of the local A^T block <= nnz
+    *bytes = L.total;
+    return IPM_OK;
+}
+
+static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspace, ipm_stream_t stream) {
+    ctx->st = reinterpret_cast<cudaStream_t>(stream);
+    ctx->n = p->n;
+    ctx->m = p->m;
+    ctx->nnz = p->nnz;
+    int64_t row0, nloc;
+    local_rows(p, row0, nloc);
+    ctx->row0 = (int)row0;
+    ctx->nloc = (int)nloc;
+    ctx->rank = p->rank;
+    ctx->nranks = std::max(1, p->nranks);
+    ctx->ws = reinterpret_cast<char *>(workspace);
+    ipm_status s = IPM_OK;
+        CK(cudaGetDevice(&ctx->device));
+        CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&ctx->hsc, sizeof(Scalars)));
+        for (auto &e : ctx->ev) CK(cudaEventCreate(&e));
+        // --- host validation of the O(n + m + nnz) data --------------------------------
+        std::vector<int64_t> rp(p->m + 1, 0);
+        std::vector<int> col(p->nnz);
+        std::vector<double> val(p->nnz), l(p->m), u(p->m), xl(p->n), xu(p->n), g(p->n);
+        if (p->m > 0) CK(cudaMemcpy(rp.data(), p->A_rowptr, sizeof(int64_t) * (p->m + 1), cudaMemcpyDeviceToHost));
+        if (p->nnz > 0) {
+            CK(cudaMemcpy(col.data(), p->A_col, sizeof(int) * p->nnz, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(val.data(), p->A_val, sizeof(double) * p->nnz, cudaMemcpyDeviceToHost));
+        }
+        if (p->m > 0) {
+            CK(cudaMemcpy(l.data(), p->l, sizeof(double) * p->m, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(u.data(), p->u, sizeof(double) * p->m, cudaMemcpyDeviceToHost));
+        }
+        CK(cudaMemcpy(xl.data(), p->xl, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(xu.data(), p->xu, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(g.data(), p->g, sizeof(double) * p->n, cudaMemcpyDeviceToHost));
+        if ((s = validate_host(ctx, p, rp, col)) != IPM_OK) return s;
+        for (double v : val)
+            if (!std::isfinite(v)) { s = fail(ctx, IPM_ERR_INVALID, "A_val has a non-finite entry"); return s; }
+        for (double v : g)
+            if (!std::isfinite(v)) { s = fail(ctx, IPM_ERR_INVALID, "g has a non-finite entry"); return s; }
+        if ((s = check_bounds(ctx, l, u, "row")) != IPM_OK) return s;
+        if ((s = check_bounds(ctx, xl, xu, "variable")) != IPM_OK) return s;
+        int64_t nb = 0;
+        for (int64_t i = 0; i < p->m; ++i) nb += std::isfinite(l[i]) + std::isfinite(u[i]);
+        for (int64_t j = 0; j < p->n; ++j) nb += std::isfinite(xl[j]) + std::isfinite(xu[j]);
+        ctx->nbounds = nb;
+
+        // --- device state ------------------------------------------------------------
+        Layout L;
+        const Offsets o = plan(nloc, p->n, p->m, p->nnz, L);
+        CK(cudaMemsetAsync(ctx->ws, 0, L.total, ctx->st));
+        ctx->sc = reinterpret_cast<Scalars *>(ctx->ws + o.sc);
+        assign_vectors(ctx, o);
+        Prob &P = ctx->P;
+        P.n = (int)nloc;
+        P.m = (int)p->m;
+        P.ncols = (int)p->n;
+        P.nnz = p->nnz;
+        P.ldh = p->ldh;
+        P.H = const_cast<double *>(p->H);
+        P.Arp = p->A_rowptr;
+        P.Acol = p->A_col;
+        P.Aval = p->A_val;
+        double *gd = reinterpret_cast<double *>(ctx->ws + o.g);
+        double *ld = reinterpret_cast<double *>(ctx->ws + o.l);
+        double *ud = reinterpret_cast<double *>(ctx->ws + o.u);
+        double *xld = reinterpret_cast<double *>(ctx->ws + o.xl);
+        double *xud = reinterpret_cast<double *>(ctx->ws + o.xu);
+        CK(cudaMemcpyAsync(gd, p->g + row0, sizeof(double) * nloc, cudaMemcpyDeviceToDevice, ctx->st));
+        CK(cudaMemcpyAsync(xld, p->xl + row0, sizeof(double) * nloc, cudaMemcpyDeviceToDevice, ctx->st));
+        CK(cudaMemcpyAsync(xud, p->xu + row0, sizeof(double) * nloc, cudaMemcpyDeviceToDevice, ctx->st));
+        if (p->m > 0) {
+            CK(cudaMemcpyAsync(ld, p->l, sizeof(double) * p->m, cudaMemcpyDeviceToDevice, ctx->st));
+            CK(cudaMemcpyAsync(ud, p->u, sizeof(double) * p->m, cudaMemcpyDeviceToDevice, ctx->st));
+        }
+        P.g = gd;
+        P.l = ld;
+        P.u = ud;
+        P.xl = xld;
+        P.xu = xud;
+        P.diagH = reinterpret_cast<double *>(ctx->ws + o.diagH);
+        int64_t *ATrp = reinterpret_cast<int64_t *>(ctx->ws + o.ATrp);
+        int *ATcol = reinterpret_cast<int *>(ctx->ws + o.ATcol);
+        double *ATval = reinterpret_cast<double *>(ctx->ws + o.ATval);
+        P.ATrp = ATrp;
+        P.ATcol = ATcol;
+        P.ATval = ATval;
+        launch_transpose(P, (int)row0, o.nchunk, reinterpret_cast<int *>(ctx->ws + o.cnt), ATrp, ATcol, ATval, ctx->st);
+        launch_setup_diag(P, (int)row0, ctx->st);
+        unsigned long long *bad = reinterpret_cast<unsigned long long *>(ctx->ws + o.bad);
+        launch_count_nonfinite(P, bad, ctx->st);
+        ctx->launches += 5;
+        CKL();
+        unsigned long long nbad = 0;
+        CK(cudaMemcpyAsync(&nbad, bad, sizeof nbad, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        if (nbad) { s = fail(ctx, IPM_ERR_INVALID, "H has %llu non-finite entries", nbad); return s; }
+        ctx->ncb = gemv_ncb((int)p->n);
+        ctx->gemv_grid = gemv_max_grid();
+        ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
+    
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_create(ipm_ctx **out, const ipm_problem *p, const ipm_options *opt, void *workspace,
+                                 size_t workspace_bytes, ipm_stream_t stream) {
+    ipm_ctx *ctx = nullptr;
+    if (!out || !p) return fail(nullptr, IPM_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (p->n < 1 || p->m < 0 || p->nnz < 0 || p->ldh < p->n)
+        return fail(nullptr, IPM_ERR_INVALID, "bad dimensions (n >= 1, m >= 0, nnz >= 0, ldh >= n)");
+    if (p->n > INT32_MAX || p->m > INT32_MAX || p->nnz >= INT32_MAX)
+        return fail(nullptr, IPM_ERR_INVALID, "dimension exceeds int32 index range");
+    if (p->nranks > 1) {
+        if (p->row_begin < 0 || p->row_end > p->n || p->row_begin >= p->row_end)
+            return fail(nullptr, IPM_ERR_INVALID, "bad row block [row_begin, row_end)");
+        return fail(nullptr, IPM_ERR_INVALID, "row-sharded path (nranks > 1) is not built in this library version");
+    }
+    if (!p->H || !p->g || !p->xl || !p->xu || (p->m > 0 && (!p->l || !p->u || !p->A_rowptr)) ||
+        (p->nnz > 0 && (!p->A_col || !p->A_val)))
+        return fail(nullptr, IPM_ERR_INVALID, "null data pointer");
+    size_t need = 0;
+    if (ipm_workspace_size(p, opt, &need) != IPM_OK) return IPM_ERR_INVALID;
+    if (!workspace || workspace_bytes < need)
+        return fail(nullptr, IPM_ERR_OOM, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(nullptr, IPM_ERR_INVALID, "workspace not 256-byte aligned");
+
+    ctx = new ipm_ctx();
+    ipm_options_default(&ctx->opt);
+    if (opt) {
+        if (opt->size != (int32_t)sizeof(ipm_options)) {
+            delete ctx;
+            return fail(nullptr, IPM_ERR_INVALID, "ipm_options.size mismatch (ABI)");
+        }
+        ctx->opt = *opt;
+    }
+    const ipm_status s = create_impl(ctx, p, workspace, stream);
+    if (s != IPM_OK) {
+        g_create_error = ctx->err;
+        ipm_destroy(ctx);
+        return s;
+    }
+    *out = ctx;
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_solve(ipm_ctx *ctx) {
+    if (!ctx) return fail(nullptr, IPM_ERR_INVALID, "null context");
+    ctx->err.clear();
+    return solve_impl(ctx);
+}
+
+IPM_EXPORT ipm_status ipm_get_solution(ipm_ctx *ctx, double *x, double *lam_lA, double *lam_uA, double *lam_lx,
+                                       double *lam_ux, double *obj_host) {
+    if (!ctx) return fail(nullptr, IPM_ERR_INVALID, "null context");
+    if (!ctx->have_iterate) return fail(ctx, IPM_ERR_STATE, "no iterate: call ipm_solve first");
+    const size_t nb = sizeof(double) * ctx->nloc, mb = sizeof(double) * ctx->m;
+    if (x) CK(cudaMemcpyAsync(x, ctx->V.x, nb, cudaMemcpyDeviceToDevice, ctx->st));
+    if (lam_lx) CK(cudaMemcpyAsync(lam_lx, ctx->V.lam_lx, nb, cudaMemcpyDeviceToDevice, ctx->st));
+    if (lam_ux) CK(cudaMemcpyAsync(lam_ux, ctx->V.lam_ux, nb, cudaMemcpyDeviceToDevice, ctx->st));
+    if (ctx->m > 0) {
+        if (lam_lA) CK(cudaMemcpyAsync(lam_lA, ctx->V.lam_lA, mb, cudaMemcpyDeviceToDevice, ctx->st));
+        if (lam_uA) CK(cudaMemcpyAsync(lam_uA, ctx->V.lam_uA, mb, cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    if (obj_host) *obj_host = ctx->stats.obj;
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_get_stats(ipm_ctx *ctx, ipm_stats *s) {
+    if (!ctx || !s) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    *s = ctx->stats;
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_get_trace(ipm_ctx *ctx, ipm_trace_rec *recs, int32_t cap, int32_t *count) {
+    if (!ctx || !count) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    const int32_t nrec = (int32_t)ctx->trace.size();
+    *count = nrec;
+    if (recs)
+        for (int32_t i = 0; i < std::min(cap, nrec); ++i) recs[i] = ctx->trace[i];
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_set_linear_term(ipm_ctx *ctx, const double *g) {
+    if (!ctx || !g) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    CK(cudaMemcpyAsync(const_cast<double *>(ctx->P.g), g + ctx->row0, sizeof(double) * ctx->nloc,
+                       cudaMemcpyDeviceToDevice, ctx->st));
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_update_hessian_rank2(ipm_ctx *ctx, const double *u, double alpha, const double *v,
+                                               double beta) {
+    if (!ctx || !u || !v) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    launch_rank2(ctx->P, ctx->row0, u, alpha, v, beta, ctx->st);
+    ctx->launches += 1;
+    CKL();
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_warm_start(ipm_ctx *ctx) {
+    if (!ctx) return fail(nullptr, IPM_ERR_INVALID, "null context");
+    if (!ctx->have_iterate) return fail(ctx, IPM_ERR_STATE, "warm start needs a previous solve");
+    ctx->warm_pending = true;
+    ctx->user_iterate = false;
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_set_iterate(ipm_ctx *ctx, const double *x, const double *const s4[4],
+                                      const double *const lam4[4], double mu) {
+    if (!ctx || !x || !s4 || !lam4) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    const Vecs &V = ctx->V;
+    double *sd[4] = {V.s_lA, V.s_uA, V.s_lx, V.s_ux};
+    double *ld[4] = {V.lam_lA, V.lam_uA, V.lam_lx, V.lam_ux};
+    for (int f = 0; f < 4; ++f) {
+        const size_t b = sizeof(double) * (f < 2 ? (size_t)ctx->m : (size_t)ctx->nloc);
+        if (b == 0) continue;
+        const size_t off = (f < 2) ? 0 : (size_t)ctx->row0;
+        CK(cudaMemcpyAsync(sd[f], s4[f] + off, b, cudaMemcpyDeviceToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ld[f], lam4[f] + off, b, cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    CK(cudaMemcpyAsync(V.x, x + ctx->row0, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
+    ctx->mu = mu;
+    ctx->user_iterate = true;
+    ctx->warm_pending = false;
+    ctx->have_iterate = true;
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_get_iterate(ipm_ctx *ctx, double *x, double *const s4[4], double *const lam4[4],
+                                      double *mu_host) {
+    if (!ctx) return fail(nullptr, IPM_ERR_INVALID, "null context");
+    if (!ctx->have_iterate) return fail(ctx, IPM_ERR_STATE, "no iterate");
+    const Vecs &V = ctx->V;
+    const double *sd[4] = {V.s_lA, V.s_uA, V.s_lx, V.s_ux};
+    const double *ld[4] = {V.lam_lA, V.lam_uA, V.lam_lx, V.lam_ux};
+    for (int f = 0; f < 4; ++f) {
+        const size_t b = sizeof(double) * (f < 2 ? (size_t)ctx->m : (size_t)ctx->nloc);
+        if (b == 0) continue;
+        if (s4 && s4[f]) CK(cudaMemcpyAsync(s4[f], sd[f], b, cudaMemcpyDeviceToDevice, ctx->st));
+        if (lam4 && lam4[f]) CK(cudaMemcpyAsync(lam4[f], ld[f], b, cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    if (x) CK(cudaMemcpyAsync(x, V.x, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
+    if (mu_host) *mu_host = ctx->mu;
+    CK(cudaStreamSynchronize(ctx->st));
+    return IPM_OK;
+}
+
+static ipm_status load_sigmas(ipm_ctx *ctx, const double *sig_b, const double *sig_c) {
+    CK(cudaMemcpyAsync(ctx->V.sig_b, sig_b, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
+    if (ctx->m > 0) CK(cudaMemcpyAsync(ctx->V.sig_c, sig_c, sizeof(double) * ctx->m, cudaMemcpyDeviceToDevice, ctx->st));
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_op_apply(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *v, double *y) {
+    if (!ctx || !sig_b || !v || !y || (ctx->m > 0 && !sig_c)) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    TRY(load_sigmas(ctx, sig_b, sig_c));
+    TRY(op_apply(ctx, v, y, nullptr, 0));
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_op_diag(ipm_ctx *ctx, const double *sig_b, const double *sig_c, double *d) {
+    if (!ctx || !sig_b || !d || (ctx->m > 0 && !sig_c)) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    TRY(load_sigmas(ctx, sig_b, sig_c));
+    launch_jacobi(ctx->P, ctx->G, ctx->V.sig_b, ctx->V.sig_c, d, 0, ctx->st);
+    ctx->launches += 1;
+    CKL();
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *rhs, double *x,
+                              double rtol, int32_t *iters) {
+    if (!ctx || !sig_b || !rhs || !x || (ctx->m > 0 && !sig_c)) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    TRY(load_sigmas(ctx, sig_b, sig_c));
+    launch_jacobi(ctx->P, ctx->G, ctx->V.sig_b, ctx->V.sig_c, ctx->V.Minv, 1, ctx->st);
+    CK(cudaMemcpyAsync(ctx->V.rhs, rhs, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
+    ctx->launches += 1;
+    PcgOut po;
+    TRY(pcg_solve(ctx, rtol, po));
+    CK(cudaMemcpyAsync(x, ctx->V.dx, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (iters) *iters = (int32_t)po.iters;
+    if (po.stalled) return fail(ctx, IPM_NOT_CONVERGED, "PCG reached its iteration limit (relres %g)", po.relres);
+    return IPM_OK;
+}
+
+IPM_EXPORT int64_t ipm_kernel_launches(const ipm_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+IPM_EXPORT const char *ipm_last_error(const ipm_ctx *ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+IPM_EXPORT void ipm_destroy(ipm_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->st) cudaStreamSynchronize(ctx->st);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->graph) cudaGraphDestroy(ctx->graph);
+    if (ctx->cap) cudaStreamDestroy(ctx->cap);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->hsc) cudaFreeHost(ctx->hsc);
+    delete ctx;
+}

@@ -1,0 +1,55 @@
+// kernels.h — launch wrappers of every kernel in libipm.so (host-callable).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "state.h"
+
+namespace ipm {
+
+constexpr int kBlock = 256;
+constexpr int kMaxGrid = 148 * 8;   // grid-stride elementwise kernels: <= 8 CTAs per SM
+constexpr int kGemvThreads = 256;   // 8 warps, 2 rows each
+constexpr int kGemvRB = 16;         // rows per GEMV tile
+constexpr int kGemvCW = 1024;       // columns per GEMV tile (8 KB of the vector in smem)
+
+inline int gemv_ncb(int ncols) { return (ncols + kGemvCW - 1) / kGemvCW; }
+
+// linalg.cu
+void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb,
+                 double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
+int gemv_max_grid();
+void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
+                 Scalars *sc, int mode, int check_done, cudaStream_t st);
+void launch_apply_reduce(const Prob &P, int G, int ncb, const double *ypart, const double *sigb,
+                         const double *v, const double *t, double *y, const double *rhs, double *dpart,
+                         Scalars *sc, int mode, cudaStream_t st);
+void launch_jacobi(const Prob &P, int G, const double *sigb, const double *sigc, double *out, int invert,
+                   cudaStream_t st);
+void launch_setup_diag(const Prob &P, int row0, cudaStream_t st);
+void launch_count_nonfinite(const Prob &P, unsigned long long *bad, cudaStream_t st);
+void launch_transpose(const Prob &P, int col0, int nchunk, int *cnt, int64_t *ATrp, int *ATcol,
+                      double *ATval, cudaStream_t st);
+void launch_rank2(const Prob &P, int row0, const double *u, double a, const double *v, double b, cudaStream_t st);
+
+// pcg.cu
+void launch_pcg_init(const Prob &P, const Vecs &V, Scalars *sc, const double *rhs, double *x, double rtol,
+                     double atol, int64_t maxit, cudaStream_t st);
+void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
+                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st);
+void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+void launch_dot2(int n, const double *a, double *dpart, Scalars *sc, cudaStream_t st);  // res2 = |a|^2
+
+// ipmops.cu — per-IPM-iteration kernels (masked full-length families)
+void launch_init_x(const Prob &P, const Vecs &V, int warm, double theta, cudaStream_t st);
+void launch_init_slacks(const Prob &P, const Vecs &V, Scalars *sc, int warm, double theta, cudaStream_t st);
+void launch_residuals(const Prob &P, const Vecs &V, int G, Scalars *sc, double mu, cudaStream_t st);
+void launch_sigma(const Prob &P, const Vecs &V, int G, cudaStream_t st);
+void launch_rhs(const Prob &P, const Vecs &V, int G, double mu, int mode, double sigma_mu, cudaStream_t st);
+void launch_recover(const Prob &P, const Vecs &V, Scalars *sc, double tau, int aff, cudaStream_t st);
+void launch_update(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+void launch_muaff(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+void launch_sum_ls(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+
+}  // namespace ipm

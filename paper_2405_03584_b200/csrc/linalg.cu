@@ -1,0 +1,442 @@
+// linalg.cu — operator-apply kernels of the condensed KKT matrix
+//
+//     K = H + Sigma_b + A^T Sigma_c A                (Schur complement of eq:2x2_reduced,
+//                                                      PAPER.md P:196-212)
+//
+// applied unassembled, block by block, as the paper does for its KKT matrix:
+//   * k_gemv_tiles  : dense row-major H times a vector.  HBM-bound (8 n^2 bytes per apply,
+//                     0.25 flop/byte — tensor cores do not apply).  2-D tiles of RB rows x CW
+//                     columns; the CW-chunk of the vector is staged once per tile in shared
+//                     memory and reused by all RB rows; H streams through 128-bit evict-first
+//                     loads with 8 independent loads in flight per lane.  Column-block partial
+//                     sums go to ypart[row][cb] (summed later in fixed order), so every tile is
+//                     independent and the persistent grid stays balanced at any n.
+//                     p^T H p is accumulated in the same pass (north_star (b)).
+//   * k_spmv        : CSR SpMV, one warp per row, lane-strided + xor-shuffle (fixed order):
+//                     the deterministic replacement of cuSPARSE CSR_ALG2 in one
+//                     kernel (no partition/fixup kernels).  Optionally scales by
+//                     Sigma_c and accumulates sum Sigma_c (A p)^2 = p^T A^T Sigma_c A p.
+//   * group SpMV^T  : A^T t through the stored transpose ("pre-compute and store their
+//                     transposes ... transpose-free SpMV"), a G-lane group per row of A^T,
+//                     fused into the consumers (PCG update, residuals, RHS, colsq).
+#include "common.cuh"
+#include "kernels.h"
+#include "state.h"
+
+namespace ipm {
+
+// ------------------------------------------------------------------------------ GEMV tiles
+template <bool VEC, int MODE>
+__global__ void __launch_bounds__(kGemvThreads)
+k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
+             const double *__restrict__ p, const double *__restrict__ pdot,
+             double *__restrict__ ypart, int ncb, double *__restrict__ dpart, Scalars *sc, int cid) {
+    __shared__ __align__(16) double ps[kGemvCW];
+    __shared__ double red[kGemvThreads / 32];
+    if (MODE == 1 && sc->done) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nrb = (nrows + kGemvRB - 1) / kGemvRB;
+    const int64_t ntiles = (int64_t)nrb * ncb;
+    double dacc = 0.0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int cb = (int)(tile % ncb), rb = (int)(tile / ncb);
+        const int c0 = cb * kGemvCW;
+        const int cw = min(kGemvCW, ncols - c0);
+        __syncthreads();
+        for (int c = threadIdx.x; c < cw; c += kGemvThreads) ps[c] = __ldg(p + c0 + c);
+        __syncthreads();
+        const int r0 = rb * kGemvRB + warp * 2;
+        if (r0 >= nrows) continue;
+        const bool two = (r0 + 1) < nrows;
+        const double *h0 = H + (int64_t)r0 * ldh + c0;
+        const double *h1 = two ? h0 + ldh : h0;
+        double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+        if (VEC) {
+            const double2 *h0v = reinterpret_cast<const double2 *>(h0);
+            const double2 *h1v = reinterpret_cast<const double2 *>(h1);
+            const double2 *pv = reinterpret_cast<const double2 *>(ps);
+            const int nv = cw >> 1;
+            int k = lane;
+            for (; k + 96 < nv; k += 128) {
+                const double2 x0 = __ldcs(h0v + k), x1 = __ldcs(h0v + k + 32);
+                const double2 x2 = __ldcs(h0v + k + 64), x3 = __ldcs(h0v + k + 96);
+                const double2 y0 = __ldcs(h1v + k), y1 = __ldcs(h1v + k + 32);
+                const double2 y2 = __ldcs(h1v + k + 64), y3 = __ldcs(h1v + k + 96);
+                const double2 q0 = pv[k], q1 = pv[k + 32], q2 = pv[k + 64], q3 = pv[k + 96];
+                a0 = fma(x0.x, q0.x, a0); b0 = fma(x0.y, q0.y, b0);
+                a1 = fma(y0.x, q0.x, a1); b1 = fma(y0.y, q0.y, b1);
+                a0 = fma(x1.x, q1.x, a0); b0 = fma(x1.y, q1.y, b0);
+                a1 = fma(y1.x, q1.x, a1); b1 = fma(y1.y, q1.y, b1);
+                a0 = fma(x2.x, q2.x, a0); b0 = fma(x2.y, q2.y, b0);
+                a1 = fma(y2.x, q2.x, a1); b1 = fma(y2.y, q2.y, b1);
+                a0 = fma(x3.x, q3.x, a0); b0 = fma(x3.y, q3.y, b0);
+                a1 = fma(y3.x, q3.x, a1); b1 = fma(y3.y, q3.y, b1);
+            }
+            for (; k < nv; k += 32) {
+                const double2 x0 = __ldcs(h0v + k), y0 = __ldcs(h1v + k);
+                const double2 q0 = pv[k];
+                a0 = fma(x0.x, q0.x, a0); b0 = fma(x0.y, q0.y, b0);
+                a1 = fma(y0.x, q0.x, a1); b1 = fma(y0.y, q0.y, b1);
+            }
+            if ((cw & 1) && lane == 0) {
+                a0 = fma(h0[cw - 1], ps[cw - 1], a0);
+                a1 = fma(h1[cw - 1], ps[cw - 1], a1);
+            }
+        } else {
+            for (int c = lane; c < cw; c += 32) {
+                const double q = ps[c];
+                a0 = fma(__ldcs(h0 + c), q, a0);
+                a1 = fma(__ldcs(h1 + c), q, a1);
+            }
+        }
+        const double s0 = warp_sum(a0 + b0);
+        const double s1 = warp_sum(a1 + b1);
+        if (lane == 0) {
+            ypart[(int64_t)r0 * ncb + cb] = s0;
+            if (pdot) dacc = fma(pdot[r0], s0, dacc);
+            if (two) {
+                ypart[(int64_t)(r0 + 1) * ncb + cb] = s1;
+                if (pdot) dacc = fma(pdot[r0 + 1], s1, dacc);
+            }
+        }
+    }
+    if (pdot == nullptr) return;
+    const double bs = block_sum(dacc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
+    if (last_block(&sc->counters[cid])) {
+        const double tot = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[cid] = 0;
+            sc->S_H = tot;
+            if (MODE == 1) {
+                const double pkp = tot + sc->S_b + sc->S_c;
+                sc->pKp = pkp;
+                if (!(pkp > 0.0) || !finite_d(pkp)) {
+                    sc->breakdown = 1;
+                    sc->done = 1;
+                    sc->alpha = 0.0;
+                } else {
+                    sc->alpha = sc->rho / pkp;
+                }
+            }
+        }
+    }
+}
+
+void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb,
+                 double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st) {
+    const bool vec = ((P.ldh & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.H) & 15) == 0);
+    if (P.n == 0) return;
+    if (mode == 1) {
+        if (vec) k_gemv_tiles<true, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+        else k_gemv_tiles<false, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+    } else {
+        if (vec) k_gemv_tiles<true, 0><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+        else k_gemv_tiles<false, 0><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+    }
+}
+
+int gemv_max_grid() {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv_tiles<true, 1>, kGemvThreads, 0);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (occ < 1) occ = 1;
+    int g = sms * occ;
+    return g > kMaxPartials ? kMaxPartials : g;
+}
+
+// ------------------------------------------------------------------------------ SpMV (A v)
+// MODE 0: y = A v.  MODE 1 (PCG): y = sig_c o (A v) and S_c = sum sig_c (A v)^2.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const double *__restrict__ val,
+       const double *__restrict__ v, const double *__restrict__ sigc, double *__restrict__ y,
+       double *__restrict__ dpart, Scalars *sc, int cid, int check_done) {
+    __shared__ double red[kBlock / 32];
+    if (check_done && sc->done) return;
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    double dacc = 0.0;
+    for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
+        const int64_t s = rp[i], e = rp[i + 1];
+        double a = 0.0;
+        for (int64_t k = s + lane; k < e; k += 32) a = fma(__ldg(val + k), __ldg(v + __ldg(col + k)), a);
+        a = warp_sum(a);
+        if (lane == 0) {
+            if (MODE == 1) {
+                const double ti = sigc[i] * a;
+                y[i] = ti;
+                dacc = fma(ti, a, dacc);
+            } else {
+                y[i] = a;
+            }
+        }
+    }
+    if (MODE == 0) return;
+    const double bs = block_sum(dacc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
+    if (last_block(&sc->counters[cid])) {
+        const double tot = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[cid] = 0;
+            sc->S_c = tot;
+        }
+    }
+}
+
+static int grid_for(int64_t units, int per_block) {
+    int64_t g = (units + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > kMaxGrid) g = kMaxGrid;
+    return (int)g;
+}
+
+void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
+                 Scalars *sc, int mode, int check_done, cudaStream_t st) {
+    if (P.m == 0) return;
+    const int grid = grid_for(P.m, kBlock / 32);
+    if (mode == 1)
+        k_spmv<1><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV_PCG, check_done);
+    else
+        k_spmv<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV, check_done);
+}
+
+// ------------------------------------------------------ y = sum_cb ypart + sig_b v + A^T t
+// MODE 0: write y.  MODE 1: r = rhs - y, res2 = ||r||^2 (true residual of PCG).
+// MODE 2: y = sum_cb ypart only (plain H v, for residuals), also obj/dots not needed.
+template <int G, int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
+               const double *__restrict__ v, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol,
+               const double *__restrict__ ATval, const double *__restrict__ t, double *__restrict__ y,
+               const double *__restrict__ rhs, double *__restrict__ dpart, Scalars *sc, int cid) {
+    __shared__ double red[kBlock / 32];
+    const int gl = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    double acc = 0.0;
+    for (int i = blockIdx.x * gpb + threadIdx.x / G; i < n; i += gridDim.x * gpb) {
+        double s = 0.0;
+        for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
+        if (MODE != 2 && t != nullptr) {
+            const int64_t e = ATrp[i + 1];
+            for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
+        }
+        s = group_sum<G>(s);
+        if (gl == 0) {
+            const double yi = (MODE == 2) ? s : fma(sigb[i], v[i], s);
+            if (MODE == 1) {
+                const double ri = rhs[i] - yi;
+                y[i] = ri;
+                acc = fma(ri, ri, acc);
+            } else {
+                y[i] = yi;
+            }
+        }
+    }
+    if (MODE != 1) return;
+    const double bs = block_sum(acc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
+    if (last_block(&sc->counters[cid])) {
+        const double tot = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[cid] = 0;
+            sc->res2 = tot;
+        }
+    }
+}
+
+#define IPM_DISPATCH_G(G, ...)                     \
+    switch (G) {                                  \
+        case 4: { constexpr int GG = 4; __VA_ARGS__; } break;   \
+        case 8: { constexpr int GG = 8; __VA_ARGS__; } break;   \
+        case 16: { constexpr int GG = 16; __VA_ARGS__; } break; \
+        default: { constexpr int GG = 32; __VA_ARGS__; } break; \
+    }
+
+void launch_apply_reduce(const Prob &P, int G, int ncb, const double *ypart, const double *sigb,
+                         const double *v, const double *t, double *y, const double *rhs, double *dpart,
+                         Scalars *sc, int mode, cudaStream_t st) {
+    if (P.n == 0) return;
+    const int grid = grid_for(P.n, kBlock / G);
+    const double *tt = (P.m > 0) ? t : nullptr;
+    if (mode == 0) {
+        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 0><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES)));
+    } else if (mode == 1) {
+        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 1><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES)));
+    } else {
+        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 2><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES)));
+    }
+}
+
+// ---------------------------------------------------- Jacobi diagonal (on device)
+// M_j = diag(H)_j + sig_b,j + sum_{k in row j of A^T} sig_c,k A_kj^2 ; writes 1/M (or M).
+template <int G>
+__global__ void __launch_bounds__(kBlock)
+k_jacobi(int n, const double *__restrict__ diagH, const double *__restrict__ sigb,
+         const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, const double *__restrict__ ATval,
+         const double *__restrict__ sigc, double *__restrict__ out, int invert) {
+    const int gl = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    for (int i = blockIdx.x * gpb + threadIdx.x / G; i < n; i += gridDim.x * gpb) {
+        double s = 0.0;
+        if (sigc != nullptr) {
+            const int64_t e = ATrp[i + 1];
+            for (int64_t k = ATrp[i] + gl; k < e; k += G) {
+                const double a = __ldg(ATval + k);
+                s = fma(a * a, __ldg(sigc + __ldg(ATcol + k)), s);
+            }
+        }
+        s = group_sum<G>(s);
+        if (gl == 0) {
+            const double d = diagH[i] + sigb[i] + s;
+            out[i] = invert ? 1.0 / d : d;
+        }
+    }
+}
+
+void launch_jacobi(const Prob &P, int G, const double *sigb, const double *sigc, double *out, int invert,
+                   cudaStream_t st) {
+    if (P.n == 0) return;
+    const int grid = grid_for(P.n, kBlock / G);
+    const double *sc = (P.m > 0) ? sigc : nullptr;
+    IPM_DISPATCH_G(G, (k_jacobi<GG><<<grid, kBlock, 0, st>>>(P.n, P.diagH, sigb, P.ATrp, P.ATcol, P.ATval, sc, out, invert)));
+}
+
+// ---------------------------------------------------------------- setup: diag(H), finiteness
+__global__ void k_diag_extract(int n, int row0, const double *__restrict__ H, int64_t ldh, double *__restrict__ d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        d[i] = H[(int64_t)i * ldh + row0 + i];
+}
+
+__global__ void k_count_nonfinite(int64_t rows, int64_t cols, const double *__restrict__ H, int64_t ldh,
+                                  unsigned long long *__restrict__ bad) {
+    unsigned long long cnt = 0;
+    const int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / cols, j = e - i * cols;
+        if (!finite_d(H[i * ldh + j])) ++cnt;
+    }
+    if (cnt) atomicAdd(bad, cnt);   // integer count: order-independent
+}
+
+void launch_setup_diag(const Prob &P, int row0, cudaStream_t st) {
+    if (P.n == 0) return;
+    k_diag_extract<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, row0, P.H, P.ldh, P.diagH);
+}
+
+void launch_count_nonfinite(const Prob &P, unsigned long long *bad, cudaStream_t st) {
+    if (P.n == 0) return;
+    k_count_nonfinite<<<kMaxGrid, kBlock, 0, st>>>(P.n, P.ncols, P.H, P.ldh, bad);
+}
+
+// --------------------------------------------------------------- setup: stored transpose A^T
+// Deterministic counting sort: rows of A are cut into nchunk contiguous chunks;
+// cnt[c][j] = #nnz of column j in chunk c (integer atomics: exact), an exclusive scan over
+// (j, c) gives every chunk its private cursor per column, then each chunk is placed by ONE
+// block walking its rows in order, so entries of every A^T row come out sorted by row
+// index — the same bits as a sequential transpose.
+__global__ void k_tr_count(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, int rows_per_chunk,
+                           int col0, int ncolsloc, int *__restrict__ cnt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const int c = i / rows_per_chunk;
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            const int j = col[k] - col0;
+            if (j >= 0 && j < ncolsloc) atomicAdd(&cnt[(int64_t)c * ncolsloc + j], 1);
+        }
+    }
+}
+
+// Single-block exclusive scan over j-major (j, c) order of cnt -> cur; ATrp[j] = start of row j.
+__global__ void k_tr_scan(int nchunk, int ncolsloc, int *__restrict__ cnt, int64_t *__restrict__ ATrp) {
+    __shared__ int64_t sh[1024];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < ncolsloc; base += blockDim.x) {
+        const int j = base + threadIdx.x;
+        int64_t tot = 0;
+        if (j < ncolsloc)
+            for (int c = 0; c < nchunk; ++c) tot += cnt[(int64_t)c * ncolsloc + j];
+        sh[threadIdx.x] = tot;
+        __syncthreads();
+        // inclusive Hillis-Steele scan in shared memory
+        for (int o = 1; o < blockDim.x; o <<= 1) {
+            const int64_t add = (threadIdx.x >= o) ? sh[threadIdx.x - o] : 0;
+            __syncthreads();
+            sh[threadIdx.x] += add;
+            __syncthreads();
+        }
+        const int64_t excl = carry + sh[threadIdx.x] - tot;
+        if (j < ncolsloc) {
+            ATrp[j] = excl;
+            int64_t run = excl;
+            for (int c = 0; c < nchunk; ++c) {
+                const int v = cnt[(int64_t)c * ncolsloc + j];
+                cnt[(int64_t)c * ncolsloc + j] = (int)run;   // cursor (fits: nnz < 2^31)
+                run += v;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += sh[threadIdx.x];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ATrp[ncolsloc] = carry;
+}
+
+__global__ void k_tr_fill(int m, const int64_t *__restrict__ rp, const int *__restrict__ col,
+                          const double *__restrict__ val, int rows_per_chunk, int col0, int ncolsloc,
+                          int *__restrict__ cur, int *__restrict__ ATcol, double *__restrict__ ATval) {
+    const int c = blockIdx.x;
+    const int i0 = c * rows_per_chunk, i1 = min(m, i0 + rows_per_chunk);
+    int *mycur = cur + (int64_t)c * ncolsloc;
+    for (int i = i0; i < i1; ++i) {
+        for (int64_t k = rp[i] + threadIdx.x; k < rp[i + 1]; k += blockDim.x) {
+            const int j = col[k] - col0;
+            if (j >= 0 && j < ncolsloc) {
+                const int pos = mycur[j]++;   // columns are distinct within a row: no conflict
+                ATcol[pos] = i;
+                ATval[pos] = val[k];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+void launch_transpose(const Prob &P, int col0, int nchunk, int *cnt, int64_t *ATrp, int *ATcol,
+                      double *ATval, cudaStream_t st) {
+    const int ncl = P.n;
+    cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)nchunk * ncl, st);
+    if (P.m > 0) {
+        const int rpc = (P.m + nchunk - 1) / nchunk;
+        k_tr_count<<<grid_for(P.m, kBlock), kBlock, 0, st>>>(P.m, P.Arp, P.Acol, rpc, col0, ncl, cnt);
+        k_tr_scan<<<1, 1024, 0, st>>>(nchunk, ncl, cnt, ATrp);
+        k_tr_fill<<<nchunk, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, rpc, col0, ncl, cnt, ATcol, ATval);
+    } else {
+        cudaMemsetAsync(ATrp, 0, sizeof(int64_t) * (size_t)(ncl + 1), st);
+    }
+}
+
+// ------------------------------------------------------------ C4: H <- H + a uu^T + b vv^T
+__global__ void k_rank2(int nrows, int row0, int ncols, double *__restrict__ H, int64_t ldh,
+                        const double *__restrict__ u, double a, const double *__restrict__ v, double b,
+                        double *__restrict__ diagH) {
+    const int64_t total = (int64_t)nrows * ncols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / ncols), j = (int)(e - (int64_t)i * ncols);
+        const int gi = row0 + i;
+        double h = H[(int64_t)i * ldh + j];
+        h = fma(a * u[gi], u[j], h);
+        h = fma(b * v[gi], v[j], h);
+        H[(int64_t)i * ldh + j] = h;
+        if (j == gi) diagH[i] = h;
+    }
+}
+
+void launch_rank2(const Prob &P, int row0, const double *u, double a, const double *v, double b, cudaStream_t st) {
+    if (P.n == 0) return;
+    k_rank2<<<kMaxGrid * 2, kBlock, 0, st>>>(P.n, row0, P.ncols, P.H, P.ldh, u, a, v, b, P.diagH);
+}
+
+}  // namespace ipm

@@ -1,0 +1,241 @@
+// pcg.cu — Jacobi-preconditioned conjugate gradients on K = H + Sigma_b + A^T Sigma_c A
+// (Alg. 1 line 2; Jacobi preconditioner P:263-268; SPEC S:222-240 contract).
+//
+// One PCG iteration = 4 kernels, all reading their scalars from device memory so the loop
+// runs without host round trips (it is captured once into a CUDA graph whose WHILE node is
+// re-armed from the device by k_pcg_update):
+//   k_pcg_p       beta = rho/rho_old (0 after a (re)start); p = z + beta p;  S_b = sum sig_b p^2
+//   k_spmv<1>     t = sig_c o (A p);                                          S_c = sum t (A p)
+//   k_gemv<1>     ypart = H p tiles;  S_H = p^T H p;  pKp = S_H+S_b+S_c;  alpha = rho/pKp
+//                 (p^T K p comes out of the SAME pass over H, north_star (b))
+//   k_pcg_update  y = sum ypart + sig_b p + A^T t;  x += alpha p;  r -= alpha y;  z = M^-1 r;
+//                 rho = r^T z; rr = r^T r; stop when rr <= tol^2, it >= maxit, breakdown.
+// All sums are fixed-order (common.cuh), so iterates are bitwise reproducible.
+#include "common.cuh"
+#include "kernels.h"
+#include "state.h"
+
+namespace ipm {
+
+static int grid_for(int64_t units, int per_block) {
+    int64_t g = (units + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > kMaxGrid) g = kMaxGrid;
+    return (int)g;
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_pcg_init(int n, const double *__restrict__ rhs, double *__restrict__ x, double *__restrict__ r,
+           double *__restrict__ z, const double *__restrict__ Minv, double *__restrict__ p1,
+           double *__restrict__ p2, double *__restrict__ p3, Scalars *sc, double rtol, double atol, int64_t maxit) {
+    __shared__ double red[kBlock / 32];
+    double rz = 0.0, rr = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double ri = rhs[i];
+        const double zi = Minv[i] * ri;
+        x[i] = 0.0;
+        r[i] = ri;
+        z[i] = zi;
+        rz = fma(ri, zi, rz);
+        rr = fma(ri, ri, rr);
+    }
+    const double a = block_sum(rz, red);
+    const double b = block_sum(rr, red);
+    if (threadIdx.x == 0) {
+        p1[blockIdx.x] = a;
+        p2[blockIdx.x] = b;
+    }
+    if (last_block(&sc->counters[C_INIT_PCG])) {
+        const double trz = sum_partials(p1, gridDim.x, red);
+        const double trr = sum_partials(p2, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_INIT_PCG] = 0;
+            sc->rho = trz;
+            sc->rho_old = trz;
+            sc->rr = trr;
+            sc->rhs2 = trr;
+            const double t1 = rtol * rtol * trr, t2 = atol * atol;
+            sc->tol2 = t1 > t2 ? t1 : t2;
+            sc->it = 0;
+            sc->it_rs = 0;
+            sc->maxit = maxit;
+            sc->breakdown = 0;
+            sc->S_b = sc->S_c = sc->S_H = 0.0;
+            sc->done = (trr <= sc->tol2) ? 1 : 0;
+            if (!finite_d(trr) || !finite_d(trz)) { sc->done = 1; sc->breakdown = 1; }
+        }
+    }
+    (void)p3;
+}
+
+void launch_pcg_init(const Prob &P, const Vecs &V, Scalars *sc, const double *rhs, double *x, double rtol,
+                     double atol, int64_t maxit, cudaStream_t st) {
+    const int grid = grid_for(P.n, kBlock);
+    k_pcg_init<<<grid, kBlock, 0, st>>>(P.n, rhs, x, V.pr, V.pz, V.Minv, V.part[0], V.part[1], V.part[2], sc, rtol,
+                                        atol, maxit);
+}
+
+// After the true-residual check (r already holds rhs - K x): z = M^-1 r, rho = r^T z, restart.
+__global__ void __launch_bounds__(kBlock)
+k_pcg_restart(int n, const double *__restrict__ r, double *__restrict__ z, const double *__restrict__ Minv,
+              double *__restrict__ p1, double *__restrict__ p2, Scalars *sc) {
+    __shared__ double red[kBlock / 32];
+    double rz = 0.0, rr = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double ri = r[i];
+        const double zi = Minv[i] * ri;
+        z[i] = zi;
+        rz = fma(ri, zi, rz);
+        rr = fma(ri, ri, rr);
+    }
+    const double a = block_sum(rz, red);
+    const double b = block_sum(rr, red);
+    if (threadIdx.x == 0) {
+        p1[blockIdx.x] = a;
+        p2[blockIdx.x] = b;
+    }
+    if (last_block(&sc->counters[C_INIT_PCG])) {
+        const double trz = sum_partials(p1, gridDim.x, red);
+        const double trr = sum_partials(p2, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_INIT_PCG] = 0;
+            sc->rho = trz;
+            sc->rho_old = trz;
+            sc->rr = trr;
+            sc->it_rs = 0;
+            sc->done = (trr <= sc->tol2 || sc->it >= sc->maxit) ? 1 : 0;
+        }
+    }
+}
+
+void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
+    k_pcg_restart<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, V.pr, V.pz, V.Minv, V.part[0], V.part[1], sc);
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_dot2(int n, const double *__restrict__ a, double *__restrict__ p1, Scalars *sc) {
+    __shared__ double red[kBlock / 32];
+    double s = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s = fma(a[i], a[i], s);
+    const double b = block_sum(s, red);
+    if (threadIdx.x == 0) p1[blockIdx.x] = b;
+    if (last_block(&sc->counters[C_TRUE_RES])) {
+        const double t = sum_partials(p1, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_TRUE_RES] = 0;
+            sc->res2 = t;
+        }
+    }
+}
+
+void launch_dot2(int n, const double *a, double *dpart, Scalars *sc, cudaStream_t st) {
+    k_dot2<<<grid_for(n, kBlock), kBlock, 0, st>>>(n, a, dpart, sc);
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_pcg_p(int n, const double *__restrict__ z, double *__restrict__ p, const double *__restrict__ sigb,
+        double *__restrict__ dpart, Scalars *sc) {
+    __shared__ double red[kBlock / 32];
+    if (sc->done) return;
+    const bool first = (sc->it_rs == 0);
+    const double beta = first ? 0.0 : sc->rho / sc->rho_old;
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double pi = first ? z[i] : fma(beta, p[i], z[i]);
+        p[i] = pi;
+        acc = fma(sigb[i] * pi, pi, acc);
+    }
+    const double b = block_sum(acc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = b;
+    if (last_block(&sc->counters[C_P])) {
+        const double t = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_P] = 0;
+            sc->S_b = t;
+        }
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kBlock)
+k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
+             const double *__restrict__ p, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol,
+             const double *__restrict__ ATval, const double *__restrict__ t, double *__restrict__ x,
+             double *__restrict__ r, double *__restrict__ z, const double *__restrict__ Minv,
+             double *__restrict__ p1, double *__restrict__ p2, Scalars *sc, cudaGraphConditionalHandle h,
+             int use_cond) {
+    __shared__ double red[kBlock / 32];
+    if (sc->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+        return;
+    }
+    const double alpha = sc->alpha;
+    const int gl = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    double rz = 0.0, rr = 0.0;
+    for (int i = blockIdx.x * gpb + threadIdx.x / G; i < n; i += gridDim.x * gpb) {
+        double s = 0.0;
+        for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
+        if (t != nullptr) {
+            const int64_t e = ATrp[i + 1];
+            for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
+        }
+        s = group_sum<G>(s);
+        if (gl == 0) {
+            const double pi = p[i];
+            const double yi = fma(sigb[i], pi, s);
+            x[i] = fma(alpha, pi, x[i]);
+            const double ri = fma(-alpha, yi, r[i]);
+            r[i] = ri;
+            const double zi = Minv[i] * ri;
+            z[i] = zi;
+            rz = fma(ri, zi, rz);
+            rr = fma(ri, ri, rr);
+        }
+    }
+    const double a = block_sum(rz, red);
+    const double b = block_sum(rr, red);
+    if (threadIdx.x == 0) {
+        p1[blockIdx.x] = a;
+        p2[blockIdx.x] = b;
+    }
+    if (last_block(&sc->counters[C_UPD])) {
+        const double trz = sum_partials(p1, gridDim.x, red);
+        const double trr = sum_partials(p2, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_UPD] = 0;
+            sc->rho_old = sc->rho;
+            sc->rho = trz;
+            sc->rr = trr;
+            sc->it += 1;
+            sc->it_rs += 1;
+            int stop = 0;
+            if (trr <= sc->tol2 || sc->it >= sc->maxit) stop = 1;
+            if (!finite_d(trr) || !finite_d(trz)) { stop = 1; sc->breakdown = 1; }
+            sc->done = stop;
+            if (use_cond) cudaGraphSetConditional(h, stop ? 0u : 1u);
+        }
+    }
+}
+
+void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
+                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
+    const int grid = grid_for(P.n, kBlock);
+    k_pcg_p<<<grid, kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2], sc);
+    launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
+    launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);
+    const int ug = grid_for(P.n, kBlock / G);
+    const double *t = (P.m > 0) ? V.pt : nullptr;
+#define IPM_UPD(GG)                                                                                              \
+    k_pcg_update<GG><<<ug, kBlock, 0, st>>>(P.n, ncb, V.ypart, V.sig_b, V.pp, P.ATrp, P.ATcol, P.ATval, t, x, V.pr, \
+                                            V.pz, V.Minv, V.part[5], V.part[6], sc, h, use_cond)
+    switch (G) {
+        case 4: IPM_UPD(4); break;
+        case 8: IPM_UPD(8); break;
+        case 16: IPM_UPD(16); break;
+        default: IPM_UPD(32); break;
+    }
+#undef IPM_UPD
+}
+
+}  // namespace ipm

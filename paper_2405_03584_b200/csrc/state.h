@@ -1,0 +1,90 @@
+// state.h — device-side views shared by the kernels and the host orchestration.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ipm {
+
+constexpr int kMaxPartials = 4096;   // per-reduction partial slots (>= any grid we launch)
+constexpr int kNumCounters = 48;
+
+// Scalars living in device memory (one struct, 8-byte fields).  Host reads a copy after
+// the per-IPM-iteration synchronisation.
+struct Scalars {
+    // --- PCG ---------------------------------------------------------------------------
+    double rho;        // r^T z of the current iteration
+    double rho_old;
+    double rr;         // r^T r
+    double tol2;       // squared stopping threshold on ||r||_2
+    double pKp;        // p^T K p
+    double alpha;      // rho / pKp
+    double S_b;        // sum sig_b p^2          (diagonal part of p^T K p)
+    double S_c;        // sum sig_c (A p)^2      (A^T Sigma_c A part)
+    double S_H;        // p^T H p
+    double rhs2;       // ||rhs||^2
+    double res2;       // scratch: a squared norm (true residual)
+    int64_t it;        // PCG iterations since the last init
+    int64_t it_rs;     // iterations since the last (re)start (beta = 0 when 0)
+    int64_t maxit;
+    int64_t done;      // 1 = stop the loop (converged or limit or breakdown)
+    int64_t breakdown; // 1 = p^T K p <= 0 or non-finite
+    // --- IPM -----------------------------------------------------------------------------
+    double sum_ls_m, sum_ls;     // sum lam*s (init / mu updates)
+    double rH_max_m, rH_max;     // (m-part unused slot kept for symmetry)
+    double prim_max_m, prim_max; // max |r_lA|,|r_uA|,|r_lx|,|r_ux|
+    double comp_max_m, comp_max; // max |lam s - mu|
+    double ls_max_m, ls_max;     // max lam s
+    double obj;                  // 1/2 x^T H x + g^T x
+    double minx_m, minl_m;       // min ratio over m-space families
+    double alpha_x, alpha_l;
+    double muaff_m, muaff;       // Mehrotra affine complementarity sums
+    int64_t nonfinite;           // residual/step contained Inf/NaN
+    unsigned int counters[kNumCounters];
+};
+
+enum Counter {
+    C_GEMV = 0, C_GEMV_PCG, C_SPMV, C_SPMV_PCG, C_P, C_UPD, C_INIT_PCG, C_TRUE_RES, C_INIT_M, C_INIT_N,
+    C_RES_M, C_RES_N, C_REC_M, C_REC_N, C_MUAFF_M, C_MUAFF_N, C_FINITE, C_LS_M, C_LS_N,
+    C_UPD2
+};
+
+// Read-only problem view.
+struct Prob {
+    int n, m;              // n = local rows of H / x-space length (== global n unsharded)
+    int ncols;             // global n (columns of H, length of gathered vectors)
+    int64_t nnz;
+    int64_t ldh;
+    double *H;             // local row block (writable only by the rank-2 update)
+    const int64_t *Arp;
+    const int *Acol;
+    const double *Aval;
+    const int64_t *ATrp;   // transpose, rows = local x-space rows
+    const int *ATcol;
+    const double *ATval;
+    const double *g, *l, *u, *xl, *xu;
+    double *diagH;
+};
+
+// Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).
+struct Vecs {
+    // n-space
+    double *x, *s_lx, *s_ux, *lam_lx, *lam_ux;
+    double *rH, *r_lx, *r_ux, *rc_lx, *rc_ux, *Hx;
+    double *sig_b, *Minv, *rhs, *dx;
+    double *ds_lx, *ds_ux, *dl_lx, *dl_ux;
+    double *ads_lx, *ads_ux, *adl_lx, *adl_ux;      // Mehrotra affine step
+    // m-space
+    double *s_lA, *s_uA, *lam_lA, *lam_uA;
+    double *r_lA, *r_uA, *rc_lA, *rc_uA, *Ax;
+    double *sig_c, *r2_l, *r2_u, *w, *Adx;
+    double *ds_lA, *ds_uA, *dl_lA, *dl_uA;
+    double *ads_lA, *ads_uA, *adl_lA, *adl_uA;
+    double *lamd;                                   // lam_lA - lam_uA scratch (m)
+    // PCG
+    double *pr, *pz, *pp, *pt, *py;                  // r, z, p (n), t (m), y (n)
+    double *ypart;                                   // n x ncb GEMV tile partials
+    double *part[8];                                 // reduction partials, kMaxPartials each
+};
+
+}  // namespace ipm

@@ -1,0 +1,83 @@
+"""CPU-only checks of the boundary: libipm.so loads, exports every entry point that
+include/ipm.h declares, and the ctypes structs match the header layout."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ipm.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2405_03584_b200 import _lib
+    return _lib
+
+
+def _declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ipm_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported(lib):
+    declared = _declared()
+    assert "ipm_create" in declared and "ipm_solve" in declared
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ipm_\w+)", out))
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    # the binding wraps exactly the declared API
+    assert sorted(lib.EXPORTED) == declared
+    # nothing else leaks out of the library (hidden visibility)
+    assert exported == set(declared)
+
+
+def test_options_default_and_abi(lib):
+    assert lib.ipm_abi_version() == 1
+    o = lib.ipm_options()
+    lib.ipm_options_default(C.byref(o))
+    assert o.size == C.sizeof(lib.ipm_options)
+    assert o.mu_tol == 1e-8 and o.tau == 0.995 and o.mu_divisor == 10.0 and o.max_ipm_iter == 100
+    assert o.pcg_rtol_max == 1e-6 and o.pcg_rtol_floor == 1e-12 and o.use_graph == 1
+
+
+def test_struct_sizes_match_c(lib, tmp_path):
+    """Compile a tiny C program against include/ipm.h and compare sizeof/offsetof with ctypes."""
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ipm.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu\\n",'
+                   'sizeof(ipm_options), sizeof(ipm_problem), sizeof(ipm_stats), sizeof(ipm_trace_rec),'
+                   'offsetof(ipm_options, warm_shift), offsetof(ipm_problem, nccl_unique_id_host));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    assert vals == [C.sizeof(lib.ipm_options), C.sizeof(lib.ipm_problem), C.sizeof(lib.ipm_stats),
+                    C.sizeof(lib.ipm_trace_rec), lib.ipm_options.warm_shift.offset,
+                    lib.ipm_problem.nccl_unique_id_host.offset]
+
+
+def test_workspace_size_host_only(lib):
+    p = lib.ipm_problem()
+    p.n, p.m, p.nnz, p.ldh, p.nranks = 20000, 5000, 10**6, 20000, 1
+    nb = C.c_size_t()
+    assert lib.ipm_workspace_size(C.byref(p), None, C.byref(nb)) == lib.IPM_OK
+    assert nb.value > 20000 * 8 * 30
+    p.n = 0
+    assert lib.ipm_workspace_size(C.byref(p), None, C.byref(nb)) == lib.IPM_ERR_INVALID
+    assert b"bad dimensions" in lib.ipm_last_error(None)
+
+
+def test_create_without_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2405_03584_b200 import QP
+    import numpy as np
+    with pytest.raises(RuntimeError):
+        QP(np.eye(2), np.zeros(2), np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0), np.zeros(0),
+           np.zeros(0), -np.ones(2), np.ones(2))

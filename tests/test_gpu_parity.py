@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Tolerances are north_star's: operator apply <= 1e-12 relative (fp64),
+final x <= 1e-6 relative, objective <= 1e-8 relative, IPM iterations within +-2."""
+import numpy as np
+import pytest
+import torch
+
+from gen.planted import config, planted_qp, random_small_qp
+from gen.torch_io import device_hessian, problem_tensors
+from oracle import kkt as okkt
+from oracle.ipm import Options, Problem, full_multipliers, solve
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0) if torch.cuda.is_available() else None
+
+
+def _qp(q, **opts):
+    from paper_2405_03584_b200 import QP
+    return QP(device=DEV, **problem_tensors(q, DEV), **opts)
+
+
+def _rand_sigmas(q, seed, dyadic=False):
+    rng = np.random.default_rng(seed)
+    if dyadic:
+        sb = rng.integers(0, 64, size=q.n) / 16.0
+        sc = rng.integers(0, 64, size=q.m) / 16.0
+        v = rng.integers(-64, 64, size=q.n) / 8.0
+    else:
+        sb = rng.uniform(0.0, 3.0, size=q.n)
+        sc = 10.0 ** rng.uniform(-3, 3, size=q.m)
+        v = rng.normal(size=q.n)
+    return sb, sc, v
+
+
+# ---------------------------------------------------------------- operator apply / diag
+@pytest.mark.parametrize("n,m,dens", [(50, 20, 0.3), (1, 1, 1.0), (1025, 300, 0.02), (3001, 0, 0.0),
+                                      (2049, 700, 0.01), (4100, 1500, 0.05)])
+def test_op_apply_matches_oracle(n, m, dens):
+    q = planted_qp(n, m, density=dens, rank=min(64, n), seed=n + m, rows="mixed" if m else "vmat",
+                   var="mixed")
+    qp = _qp(q)
+    sb, sc, v = _rand_sigmas(q, 1)
+    y = qp.op_apply(sb, sc, v).cpu().numpy()
+    A = q.A_dense()
+    yref = okkt.condensed_apply(q.H, A, sb, sc, v, dtype=np.longdouble)
+    err = np.linalg.norm((y - yref).astype(np.float64)) / np.linalg.norm(yref.astype(np.float64))
+    assert err <= 1e-12, err
+    d = qp.op_diag(sb, sc).cpu().numpy()
+    dref = okkt.jacobi_diag(q.H, A, sb, sc)
+    assert np.max(np.abs(d - dref) / np.abs(dref)) <= 1e-13
+
+
+def test_op_apply_bit_exact_on_dyadic_inputs():
+    """Every product and partial sum exact in fp64 -> GPU == numpy bit for bit, whatever the
+    summation order (SURVEY.md §8(c) 'Operator apply')."""
+    q = planted_qp(1500, 400, density=0.02, rank=32, seed=9, rows="mixed")
+    q.A_val = np.round(q.A_val * 16) / 16.0
+    qp = _qp(q)
+    sb, sc, v = _rand_sigmas(q, 2, dyadic=True)
+    y = qp.op_apply(sb, sc, v).cpu().numpy()
+    yref = okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v)
+    assert np.array_equal(y, yref)
+
+
+def test_device_hessian_bitwise_equals_numpy():
+    q = planted_qp(777, 0, rank=64, seed=4)
+    H, ldh = device_hessian(q, DEV)
+    assert np.array_equal(H[:, :q.n].cpu().numpy(), q.H)
+
+
+# ---------------------------------------------------------------- PCG
+def test_pcg_identity_and_jacobi_exact():
+    """K = I converges in 1 iteration; diagonal K with Jacobi in 1."""
+    n = 64
+    d = np.zeros(n)
+    q = planted_qp(n, 0, rank=1, seed=0)
+    q.U[:] = 0.0
+    q.d[:] = 1.0
+    q._H = None
+    qp = _qp(q)
+    rhs = np.random.default_rng(0).normal(size=n)
+    x, it = qp.pcg(np.zeros(n), np.zeros(0), rhs, 1e-12)
+    assert it == 1 and np.allclose(x.cpu().numpy(), rhs, rtol=0, atol=1e-14)
+    x, it = qp.pcg(np.arange(1.0, n + 1) - 1.0, np.zeros(0), rhs, 1e-12)   # K = diag(1..n)
+    assert it == 1
+    assert np.max(np.abs(x.cpu().numpy() - rhs / np.arange(1.0, n + 1))) <= 1e-14
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_pcg_solves_condensed_system(seed):
+    q = planted_qp(800, 300, density=0.03, rank=48, seed=seed, rows="mixed", var="mixed")
+    qp = _qp(q)
+    sb, sc, _ = _rand_sigmas(q, seed)
+    sc = np.minimum(sc, 10.0)
+    K = okkt.condensed_matrix(q.H, q.A_dense(), sb, sc)
+    rhs = np.random.default_rng(seed).normal(size=q.n)
+    x, it = qp.pcg(sb, sc, rhs, 1e-10)
+    x = x.cpu().numpy()
+    assert np.linalg.norm(rhs - K @ x) <= 1.0000001e-10 * np.linalg.norm(rhs)
+    xref = np.linalg.solve(K, rhs)
+    assert np.max(np.abs(x - xref)) <= 1e-6 * np.max(np.abs(xref))
+
+
+def test_pcg_deterministic():
+    q = planted_qp(2000, 500, density=0.02, rank=32, seed=3)
+    qp = _qp(q)
+    sb, sc, _ = _rand_sigmas(q, 5)
+    rhs = np.random.default_rng(1).normal(size=q.n)
+    x1, i1 = qp.pcg(sb, sc, rhs, 1e-9)
+    x2, i2 = qp.pcg(sb, sc, rhs, 1e-9)
+    assert i1 == i2 and torch.equal(x1, x2)
+
+
+# ---------------------------------------------------------------- whole IPM vs oracle
+def _check_against_oracle(q, opts_gpu=None, opts_or=None, xtol=1e-6, ftol=1e-8, ittol=2):
+    qp = _qp(q, **(opts_gpu or {}))
+    status = qp.solve()
+    sol = qp.solution()
+    st = qp.stats()
+    ref = solve(Problem.from_data(q), opts_or or Options())
+    x = sol["x"].cpu().numpy()
+    assert status == "ok" and ref.status == "converged", (status, st)
+    assert np.max(np.abs(x - ref.x)) <= xtol * max(1.0, np.max(np.abs(ref.x))), np.max(np.abs(x - ref.x))
+    assert abs(sol["obj"] - ref.obj) <= ftol * max(1.0, abs(ref.obj))
+    assert abs(st["ipm_iters"] - ref.iters) <= ittol, (st["ipm_iters"], ref.iters)
+    return qp, sol, st, ref
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_ipm_C1_matches_oracle(seed):
+    q = config("C1", seed)
+    _, sol, _, _ = _check_against_oracle(q)
+    assert np.max(np.abs(sol["x"].cpu().numpy() - q.x_star)) <= 1e-6 * np.max(np.abs(q.x_star))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_ipm_random_small_matches_oracle(seed):
+    q = random_small_qp(12, 8, seed, density=0.5)
+    _check_against_oracle(q)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_ipm_mehrotra_matches_oracle(seed):
+    q = config("C1", seed)
+    _check_against_oracle(q, dict(predictor_corrector=1), Options(predictor_corrector=True))
+
+
+def test_ipm_medium_planted_and_oracle():
+    q = planted_qp(1200, 400, density=0.02, rank=48, seed=7, rows="vmat", var="box")
+    qp, sol, st, ref = _check_against_oracle(q)
+    assert abs(sol["obj"] - q.f_star) <= 1e-8 * abs(q.f_star)
+
+
+def test_ipm_box_only_and_odd_n():
+    q = planted_qp(1537, 0, rank=40, seed=2, var="box")
+    _check_against_oracle(q)
+
+
+def test_ipm_no_bounds_one_step():
+    q = planted_qp(300, 0, rank=50, seed=1, var="none")
+    qp = _qp(q)
+    assert qp.solve() == "ok"
+    assert qp.stats()["ipm_iters"] == 1
+    x = qp.solution()["x"].cpu().numpy()
+    xcf = np.linalg.solve(q.H, -q.g)
+    assert np.max(np.abs(x - xcf)) <= 1e-9 * np.max(np.abs(xcf))
+
+
+def test_ipm_deterministic_bitwise():
+    q = planted_qp(900, 300, density=0.03, rank=32, seed=5, rows="mixed", var="mixed")
+    qp = _qp(q, trace=1)
+    qp.solve()
+    x1 = qp.solution()["x"].clone()
+    t1 = qp.trace()
+    qp.solve()
+    x2 = qp.solution()["x"].clone()
+    assert torch.equal(x1, x2) and t1 == qp.trace()
+
+
+def test_host_loop_fallback_equals_graph():
+    q = config("C1", 3)
+    a = _qp(q, use_graph=1)
+    b = _qp(q, use_graph=0)
+    a.solve()
+    b.solve()
+    assert torch.equal(a.solution()["x"], b.solution()["x"])
+
+
+# ---------------------------------------------------------------- validation / errors
+def test_invalid_inputs_rejected():
+    from paper_2405_03584_b200 import QP, _lib
+    q = config("C1", 0)
+    t = problem_tensors(q, DEV)
+    bad = dict(t)
+    col = t["A_col"].clone()
+    col[1], col[0] = col[0].item(), col[1].item()   # unsorted row
+    bad["A_col"] = col
+    with pytest.raises(_lib.IpmError, match="strictly increasing"):
+        QP(device=DEV, **bad)
+    bad = dict(t)
+    l = t["l"].clone()
+    i = int(torch.nonzero(torch.isfinite(t["l"]) & torch.isfinite(t["u"]))[0])
+    l[i] = t["u"][i]
+    bad["l"] = l
+    with pytest.raises(_lib.IpmError, match="lower < upper"):
+        QP(device=DEV, **bad)
+    bad = dict(t)
+    H = t["H"].clone()
+    H[3, 7] = float("nan")
+    bad["H"] = H
+    with pytest.raises(_lib.IpmError, match="non-finite"):
+        QP(device=DEV, **bad)
