@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (BASELINE.json metric) — one JSON line on rank 0.
+
+A *step* is one full QP solve (Algorithm 1 to convergence, every §8(a) row: initial point,
+residuals, diagonals + Jacobi, RHS, the PCG solve, recovery, step lengths, update) of the
+workload, cold-started, with all inputs resident in HBM.  Default workload: C3, the
+patient-case-shaped QP (n=20000, m=5000, 1% dense A, dense 3.2 GB H) — see DESIGN.md §7.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl ours|reference]
+
+value = QPs solved per second over the whole job (all ranks) = N*K / max-over-ranks time.
+N > 1 runs independent replicas (one QP per rank; "scaling": "weak") until the row-sharded
+C5 path is wired into the bench.  --impl reference times the CPU oracle (oracle/) as it
+stands on the host cores, on a bounded sample (one IPM iteration per step) scaled to QP/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QP solve time (s) & PCG it/s at 1/2/4/8 B200; op-apply HBM GB/s vs peak"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- oracle
+def oracle_sample(workload: str, seed: int, iters: int = 1):
+    """Time `iters` IPM iterations of the CPU oracle (as it stands) on the workload and
+    return (seconds per IPM iteration, cores, description)."""
+    import numpy as np  # noqa: F401
+    from gen.planted import config
+    from oracle.ipm import Options, Problem, initial_point, max_step, newton_direction, residuals
+    q = config(workload, seed)
+    p = Problem.from_data(q)
+    opt = Options()
+    it = initial_point(p, opt)
+    r = residuals(p, it)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        dx, ds, dl = newton_direction(p, it, r)
+        ax = max_step(it.s, ds, opt.tau)
+        al = max_step(it.lam, dl, opt.tau)
+        it.x = it.x + ax * dx
+        for f in ds:
+            it.s[f] = it.s[f] + ax * ds[f]
+            it.lam[f] = it.lam[f] + al * dl[f]
+        r = residuals(p, it)
+    dt = (time.perf_counter() - t0) / iters
+    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", "0")) or os.cpu_count()
+    return dt, cores
+
+
+def oracle_ipm_iters(workload: str, seed: int):
+    path = os.path.join(ROOT, "tests", "golden", "oracle_counts.json")
+    if os.path.exists(path):
+        d = json.load(open(path)).get(f"{workload}/seed{seed}")
+        if d:
+            return int(d["ipm_iters"]), "tests/golden/oracle_counts.json (full oracle run)"
+    return None, None
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    n_ipm, src = oracle_ipm_iters(args.workload, args.seed)
+    times = []
+    for _ in range(args.warmup if args.warmup < 1 else 0):
+        pass
+    cores = None
+    for k in range(args.steps):
+        dt, cores = oracle_sample(args.workload, args.seed, 1)
+        times.append(dt)
+    t_iter = statistics.median(times)
+    if n_ipm is None:
+        n_ipm, src = 20, "assumed 20 IPM iterations (no stored oracle count)"
+    qp_s = t_iter * n_ipm
+    sample = (f"1 oracle IPM iteration (dense Cholesky of K, n={args.workload}) per step, median of {len(times)}; "
+              f"QP time = {t_iter:.2f} s/iter x {n_ipm} IPM iterations [{src}]")
+    line = {"impl": "reference", "metric": METRIC, "value": 1.0 / qp_s, "unit": "QP/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": qp_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/planted.py, seeded)",
+            "config": {"workload": args.workload, "seed": args.seed},
+            "cpu_baseline": {"value": 1.0 / qp_s, "unit": "QP/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": 1.0 / qp_s, "unit": "QP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "qp_solve_s": qp_s, "oracle_s_per_ipm_iter": t_iter}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from gen.planted import CONFIGS, config
+    from gen.torch_io import problem_tensors
+    from paper_2405_03584_b200 import QP
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    q = config(args.workload, args.seed)
+    n, m, nnz = q.n, q.m, q.nnz
+    t = problem_tensors(q, dev)
+    torch.cuda.synchronize()
+    qp = QP(device=dev, **t)
+    stream = qp.stream
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        qp.solve()
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    stats = []
+    launches0 = qp.kernel_launches()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        status = qp.solve()
+        stats.append(qp.stats())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = qp.kernel_launches() - launches0
+    t_s = e0.elapsed_time(e1) / 1e3
+    tt = torch.tensor([t_s], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max = float(tt.item())
+    pcg_total = sum(s["pcg_iters_total"] for s in stats)
+    pcg_ms = sum(s["t_pcg_ms"] for s in stats)
+    ipm_iters = [s["ipm_iters"] for s in stats]
+    statuses = sorted(set(s["status"] for s in stats))
+
+    # --- roofline of the dominant kernel (the PCG GEMV), CUDA events on our stream -------
+    gemv_ms = qp.profile("gemv", reps=10 if n >= 10000 else 50)
+    pcg_iter_ms = qp.profile("pcg_iter", reps=10 if n >= 10000 else 50)
+    gemv_bytes = 8.0 * n * n + 8.0 * n + 8.0 * n * ((n + 1023) // 1024)   # H + p + tile partials
+    peak, peak_src = _peaks()
+    achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp)).get(args.workload)
+        if tj:
+            traffic = tj.get("dram_bytes_per_launch")
+    iter_bytes = gemv_bytes + 2 * 12.0 * nnz + 8.0 * (m + 1) + 8.0 * (n + 1) + 8.0 * 2 * m + 8.0 * 12 * n
+
+    # --- end to end through the public API with host buffers ----------------------------
+    th = problem_tensors(q, dev, host=True)
+    h2d = sum(v.numel() * v.element_size() for k, v in th.items() if hasattr(v, "numel"))
+    e2e_times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        a0 = time.perf_counter()
+        qp2 = QP(device=dev, **th)            # H2D of every input (pinned), validation, A^T build
+        qp2.solve()
+        x_host = qp2.solution()["x"].cpu()   # D2H of the result
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - a0)
+        qp2.close()
+        del qp2
+    e2e_t = sum(e2e_times)
+    te = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    d2h = n * 8
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        n_ipm, src = oracle_ipm_iters(args.workload, args.seed)
+        if n_ipm is None:
+            n_ipm, src = int(round(statistics.mean(ipm_iters))), "IPM count of this GPU run (parity +-2)"
+        dt, cores = oracle_sample(args.workload, args.seed, 1)
+        cpu = {"value": 1.0 / (dt * n_ipm), "unit": "QP/s", "cores": cores, "kind": "oracle",
+               "sample": f"1 oracle IPM iteration of {args.workload} seed {args.seed} ({dt:.1f} s, dense Cholesky "
+                         f"of K on {cores} host threads) x {n_ipm} IPM iterations [{src}]"}
+
+    if rank == 0:
+        qps = ws * args.steps / t_max
+        line = {
+            "metric": METRIC, "value": qps, "unit": "QP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic planted-KKT QP (gen/planted.py, seeded; random-init dyadic H = diag + U W U^T)",
+            "config": {"workload": args.workload, **CONFIGS[args.workload], "seed": args.seed, "nnz": nnz,
+                       "H_bytes": 8 * n * n, "l2": "inputs larger than L2 (H >> 126 MB), no flush",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "qp_solve_s": t_max / args.steps,
+            "pcg_it_per_s": pcg_total / (pcg_ms * 1e-3) if pcg_ms > 0 else None,
+            "pcg_iters_per_qp": pcg_total / args.steps, "ipm_iters": ipm_iters, "status": statuses,
+            "pcg_iter_us_isolated": pcg_iter_ms * 1e3,
+            "op_apply_GBps": iter_bytes / (pcg_iter_ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "k_gemv_tiles<VEC,1> (PCG GEMV, p^T H p fused)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "algorithmic_bytes_per_launch": gemv_bytes,
+                         "launch_ms": gemv_ms, "peak_source": peak_src,
+                         "timing": "CUDA events on the library stream, back-to-back launches after the timed region"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": ws * args.steps / float(te.item()), "unit": "QP/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    qp.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C3", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -76,6 +76,7 @@ typedef struct {
     int32_t trace;              /* 1: record one ipm_trace_rec per IPM iteration */
     int32_t use_graph;          /* 1: PCG loop as a CUDA graph with a device-side WHILE node */
     double warm_shift;          /* 1e-3   theta of the warm-start rule (R15) */
+    int32_t gemv_kernel;        /* 0 auto, 1 LDG.128 register tiles, 2 TMA-bulk mbarrier pipeline */
 } ipm_options;
 
 /* Problem description for ipm_create.  Large arrays are BORROWED (the caller keeps them
@@ -177,6 +178,13 @@ ipm_status ipm_op_apply(ipm_ctx *ctx, const double *sig_b, const double *sig_c, 
 ipm_status ipm_op_diag(ipm_ctx *ctx, const double *sig_b, const double *sig_c, double *d);
 ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *rhs,
                    double *x, double rtol, int32_t *iters_host);
+
+/* Measurement hook (bench.py roofline): launch one hot-path stage `reps` times back to back
+ * on the context's stream, bracketed by CUDA events recorded on that stream, with the
+ * current PCG vectors as operands; *ms_host = average device time per launch.
+ *   what = 0: the PCG GEMV kernel (y-tiles of H p + p^T H p), 1: the PCG SpMV (A p),
+ *   what = 2: one full PCG iteration (all four kernels).  Clobbers PCG scratch state. */
+ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, double *ms_host);
 
 /* Number of kernel launches the library issued since create (graph nodes count once per
  * executed node); used by bench.py's gpu_launches. */

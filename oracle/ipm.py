@@ -45,6 +45,7 @@ from typing import Dict, List, Optional
 
 import numpy as np
 import scipy.linalg as sla
+import scipy.sparse as sp
 
 FAMILIES = ("lA", "uA", "lx", "ux")
 
@@ -62,16 +63,18 @@ class Options:
 
 @dataclasses.dataclass
 class Problem:
-    """Dense/compact view of the QP used by the oracle."""
+    """The QP as the oracle sees it: dense H, sparse A (scipy CSR; a library container,
+    no arithmetic of the method), and the four bound families in compact form."""
     H: np.ndarray
     g: np.ndarray
-    A: np.ndarray            # dense m x n (oracle sizes are small enough)
+    A: "sp.csr_matrix"       # m x n
     l: np.ndarray
     u: np.ndarray
     xl: np.ndarray
     xu: np.ndarray
 
     def __post_init__(self):
+        self.A = sp.csr_matrix(self.A)
         self.n = self.H.shape[0]
         self.m = self.A.shape[0]
         # index sets of finite bounds (R10)
@@ -79,8 +82,8 @@ class Problem:
         self.I_u = np.flatnonzero(np.isfinite(self.u))
         self.J_l = np.flatnonzero(np.isfinite(self.xl))
         self.J_u = np.flatnonzero(np.isfinite(self.xu))
-        # constraint "matrices" of each family: rows of A, or rows of the identity
-        I = np.eye(self.n)
+        # constraint matrix of each family: rows of A, or rows of the identity
+        I = sp.identity(self.n, format="csr")
         self.C = {"lA": self.A[self.I_l], "uA": self.A[self.I_u],
                   "lx": I[self.J_l], "ux": I[self.J_u]}
         self.bound = {"lA": self.l[self.I_l], "uA": self.u[self.I_u],
@@ -89,8 +92,11 @@ class Problem:
 
     @staticmethod
     def from_data(q, H: Optional[np.ndarray] = None) -> "Problem":
-        return Problem(H=q.H if H is None else H, g=q.g.copy(), A=q.A_dense(), l=q.l.copy(),
+        return Problem(H=q.H if H is None else H, g=q.g.copy(), A=q.A_scipy(), l=q.l.copy(),
                        u=q.u.copy(), xl=q.xl.copy(), xu=q.xu.copy())
+
+    def A_dense(self) -> np.ndarray:
+        return self.A.toarray()
 
     def objective(self, x):
         return 0.5 * float(x @ (self.H @ x)) + float(self.g @ x)
@@ -203,10 +209,12 @@ def reduced_system(p: Problem, it: Iterate, r: Dict[str, np.ndarray]):
         r2 = ( -r_lA - Lam_lA^-1 r_c,lA ;  -r_uA - Lam_uA^-1 r_c,uA ).
     """
     s, lam = it.s, it.lam
+    # S_lx^-1 Lam_lx + S_ux^-1 Lam_ux is diagonal: C_f^T diag(v) C_f = diag(C_f^T v) for the
+    # identity-row families, so Q = H + diag(sigma_b).
+    sigma_b = p.C["lx"].T @ (lam["lx"] / s["lx"]) + p.C["ux"].T @ (lam["ux"] / s["ux"])
     Q = p.H.copy()
-    Q += p.C["lx"].T @ np.diag(lam["lx"] / s["lx"]) @ p.C["lx"]
-    Q += p.C["ux"].T @ np.diag(lam["ux"] / s["ux"]) @ p.C["ux"]
-    B = np.vstack([p.C["lA"], -p.C["uA"]])
+    Q[np.diag_indices(p.n)] += sigma_b
+    B = sp.vstack([p.C["lA"], -p.C["uA"]], format="csr")
     D = np.concatenate([s["lA"] / lam["lA"], s["uA"] / lam["uA"]])
     r1 = -r["H"].copy()
     r1 -= p.C["lx"].T @ ((r["clx"] + lam["lx"] * r["lx"]) / s["lx"])
@@ -219,7 +227,7 @@ def condensed_solve(Q, B, D, r1, r2):
     """Exact solve of eq:2x2_reduced through its Schur complement (D1):
        (Q + B^T D^-1 B) dx = r1 + B^T D^-1 r2 ;  dlam_A = D^-1 (r2 - B dx).
     The matrix is SPD (Q SPD, D > 0); a Cholesky failure is an error."""
-    K = Q + B.T @ (B / D[:, None])
+    K = Q + (B.T @ sp.diags(1.0 / D) @ B).toarray()
     rhs = r1 + B.T @ (r2 / D)
     c = sla.cho_factor(K, lower=True, check_finite=True)
     dx = sla.cho_solve(c, rhs)

@@ -23,7 +23,8 @@ from .ipm import FAMILIES, Iterate, Problem
 
 def full_newton_step(p: Problem, it: Iterate, r):
     n = p.n
-    sizes = [p.C[f].shape[0] for f in FAMILIES]
+    Cd = {f: p.C[f].toarray() for f in FAMILIES}     # tiny sizes: dense blocks
+    sizes = [Cd[f].shape[0] for f in FAMILIES]
     nl = sum(sizes)
     N = n + 2 * nl
     Kf = np.zeros((N, N))
@@ -41,13 +42,13 @@ def full_newton_step(p: Problem, it: Iterate, r):
     Kf[:n, :n] = p.H
     sign = {"lA": -1.0, "uA": 1.0, "lx": -1.0, "ux": 1.0}
     for f, sz in zip(FAMILIES, sizes):
-        Kf[:n, off_l[f]:off_l[f] + sz] = sign[f] * p.C[f].T
+        Kf[:n, off_l[f]:off_l[f] + sz] = sign[f] * Cd[f].T
     rhs[:n] = -r["H"]
     # primal rows: lower families  C dx - ds = -r ;  upper families  -C dx - ds = -r
     row = n
     for f, sz in zip(FAMILIES, sizes):
         sg = 1.0 if f in ("lA", "lx") else -1.0
-        Kf[row:row + sz, :n] = sg * p.C[f]
+        Kf[row:row + sz, :n] = sg * Cd[f]
         Kf[row:row + sz, off_s[f]:off_s[f] + sz] = -np.eye(sz)
         rhs[row:row + sz] = -r[f]
         row += sz
@@ -65,6 +66,7 @@ def full_newton_step(p: Problem, it: Iterate, r):
 
 
 def doubly_augmented_solve(Q, B, D, r1, r2):
+    B = B.toarray() if hasattr(B, "toarray") else B
     n = Q.shape[0]
     mA = B.shape[0]
     Dinv = 1.0 / D

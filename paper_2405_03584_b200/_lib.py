@@ -30,7 +30,7 @@ class ipm_options(C.Structure):
                 ("pcg_schedule", C.c_int32), ("pcg_rtol_max", C.c_double), ("pcg_rtol_mu_factor", C.c_double),
                 ("pcg_rtol_floor", C.c_double), ("pcg_atol", C.c_double), ("pcg_max_iter", C.c_int32),
                 ("predictor_corrector", C.c_int32), ("trace", C.c_int32), ("use_graph", C.c_int32),
-                ("warm_shift", C.c_double)]
+                ("warm_shift", C.c_double), ("gemv_kernel", C.c_int32)]
 
 
 class ipm_problem(C.Structure):
@@ -74,6 +74,7 @@ _sigs = {
     "ipm_op_apply": ([_P, _P, _P, _P, _P], _S),
     "ipm_op_diag": ([_P, _P, _P, _P], _S),
     "ipm_pcg": ([_P, _P, _P, _P, _P, _D, C.POINTER(C.c_int32)], _S),
+    "ipm_profile": ([_P, C.c_int32, C.c_int32, C.POINTER(_D)], _S),
     "ipm_kernel_launches": ([_P], C.c_int64),
     "ipm_last_error": ([_P], C.c_char_p),
     "ipm_destroy": ([_P], None),

@@ -27,6 +27,23 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// IPM_DEBUG=1 in the environment prints host-side progress to stderr (diagnostics only).
+bool dbg() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("IPM_DEBUG");
+        v = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+#define DBG(...)                                  \
+    do {                                          \
+        if (dbg()) {                              \
+            fprintf(stderr, "[ipm] " __VA_ARGS__); \
+            fflush(stderr);                       \
+        }                                         \
+    } while (0)
+
 struct Layout {
     size_t total = 0;
     size_t take(size_t bytes) {
@@ -186,9 +203,15 @@ double pcg_rtol(const ipm_options &o, double mu) {
 
 // ---------------------------------------------------------------------------- operators
 // y = K v with the current sig_b/sig_c (t and ypart are scratch).  mode 1: r = rhs - K v.
-ipm_status op_apply(ipm_ctx *ctx, const double *v, double *out, const double *rhs, int mode) {
+ipm_status op_apply(ipm_ctx *ctx, const double *v_in, double *out, const double *rhs, int mode) {
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
+    // the operand must live in the workspace (16-B aligned, padded): copy caller vectors
+    const double *v = v_in;
+    if (v_in != V.dx && v_in != V.x && v_in != V.pp) {
+        CK(cudaMemcpyAsync(V.py, v_in, sizeof(double) * P.n, cudaMemcpyDeviceToDevice, ctx->st));
+        v = V.py;
+    }
     launch_spmv(P, v, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 0, ctx->st);
     launch_gemv(P, v, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
     launch_apply_reduce(P, ctx->G, ctx->ncb, V.ypart, V.sig_b, v, V.pt, out, rhs, V.part[5], ctx->sc, mode, ctx->st);
@@ -246,11 +269,14 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
                 for (int b = 0; b < 16; ++b)
                     launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st);
                 TRY(sync_scalars(ctx));
+                DBG("  host batch: it=%lld rr=%.3e done=%lld\n", (long long)ctx->hsc->it, ctx->hsc->rr, (long long)ctx->hsc->done);
                 ctx->launches += 16 * (3 + (P.m > 0 ? 1 : 0));
                 if (ctx->hsc->done) break;
             }
         }
         const Scalars &h = *ctx->hsc;
+        DBG("pcg round %d: it=%lld rr=%.3e tol2=%.3e done=%lld breakdown=%lld rho=%.3e pKp=%.3e\n", round,
+            (long long)h.it, h.rr, h.tol2, (long long)h.done, (long long)h.breakdown, h.rho, h.pKp);
         if (ctx->opt.use_graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * (3 + (P.m > 0 ? 1 : 0));
         it_prev = h.it;
         if (h.breakdown) {
@@ -348,6 +374,7 @@ ipm_status solve_impl(ipm_ctx *ctx) {
     ipm_status status = IPM_NOT_CONVERGED;
     const bool pc = o.predictor_corrector && ctx->nbounds > 0;
     int k = 0;
+    DBG("solve start: n=%d m=%d mu0=%.3e kkt=%.3e\n", ctx->P.n, ctx->P.m, mu, kkt_inf(*ctx->hsc));
     for (k = 1; k <= o.max_ipm_iter; ++k) {
         launch_sigma(ctx->P, ctx->V, ctx->G, ctx->st);
         ctx->launches += 1 + (ctx->P.m > 0 ? 1 : 0);
@@ -382,6 +409,8 @@ ipm_status solve_impl(ipm_ctx *ctx) {
         S.pcg_iters_max = std::max<int32_t>(S.pcg_iters_max, (int32_t)std::max(po.iters, po2.iters));
         S.pcg_stalls += (po.stalled ? 1 : 0) + (po2.stalled ? 1 : 0);
         S.pcg_restarts += po.restarts + po2.restarts;
+        DBG("ipm it %d: mu=%.3e kkt=%.3e (rH %.2e prim %.2e comp %.2e) ax=%.3f al=%.3f pcg=%lld obj=%.10e\n", k, mu,
+            kkt_inf(h), h.rH_max, h.prim_max, h.comp_max, h.alpha_x, h.alpha_l, (long long)its, h.obj);
         if (h.nonfinite) {
             status = fail(ctx, IPM_ERR_NONFINITE, "non-finite residual or step at IPM iteration %d", k);
             break;
@@ -612,6 +641,10 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         if (nbad) { s = fail(ctx, IPM_ERR_INVALID, "H has %llu non-finite entries", nbad); return s; }
         ctx->ncb = gemv_ncb((int)p->n);
         ctx->gemv_grid = gemv_max_grid();
+        const int gk = ctx->opt.gemv_kernel;
+        P.gemv_bulk = (gk == 2 || gk == 0) && gemv_bulk_ok(P) ? 1 : 0;
+        if (gk == 2 && !P.gemv_bulk) { s = fail(ctx, IPM_ERR_INVALID, "gemv_kernel=2 needs even ldh and 16-byte aligned H"); return s; }
+        P.gemv_bulk_grid = gemv_bulk_grid();
         ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
     
     return IPM_OK;
@@ -795,6 +828,33 @@ IPM_EXPORT ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *s
     CK(cudaStreamSynchronize(ctx->st));
     if (iters) *iters = (int32_t)po.iters;
     if (po.stalled) return fail(ctx, IPM_NOT_CONVERGED, "PCG reached its iteration limit (relres %g)", po.relres);
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, double *ms) {
+    if (!ctx || !ms || reps < 1 || what < 0 || what > 2) return fail(ctx, IPM_ERR_INVALID, "bad argument");
+    const Prob &P = ctx->P;
+    const Vecs &V = ctx->V;
+    CK(cudaMemsetAsync(&ctx->sc->done, 0, sizeof(int64_t), ctx->st));
+    CK(cudaMemsetAsync(&ctx->sc->it_rs, 0, sizeof(int64_t), ctx->st));
+    auto one = [&]() {
+        if (what == 0) launch_gemv(P, V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, ctx->st);
+        else if (what == 1) launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
+        else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st);
+    };
+    one();  // warm-up
+    CK(cudaEventRecord(ctx->ev[2], ctx->st));
+    for (int i = 0; i < reps; ++i) {
+        if (what == 2) CK(cudaMemsetAsync(&ctx->sc->done, 0, sizeof(int64_t), ctx->st));
+        one();
+    }
+    CK(cudaEventRecord(ctx->ev[3], ctx->st));
+    CKL();
+    CK(cudaEventSynchronize(ctx->ev[3]));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]));
+    *ms = (double)t / reps;
+    ctx->launches += (int64_t)(reps + 1) * (what == 2 ? (3 + (P.m > 0)) : 1);
     return IPM_OK;
 }
 

@@ -20,6 +20,10 @@ inline int gemv_ncb(int ncols) { return (ncols + kGemvCW - 1) / kGemvCW; }
 void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb,
                  double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
 int gemv_max_grid();
+bool gemv_bulk_ok(const Prob &P);
+int gemv_bulk_grid();
+void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb, double *dpart,
+                      Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
                  Scalars *sc, int mode, int check_done, cudaStream_t st);
 void launch_apply_reduce(const Prob &P, int G, int ncb, const double *ypart, const double *sigb,

@@ -127,6 +127,10 @@ void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypa
                  double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st) {
     const bool vec = ((P.ldh & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.H) & 15) == 0);
     if (P.n == 0) return;
+    if (P.gemv_bulk) {
+        launch_gemv_bulk(P, v, vdot, ypart, ncb, dpart, sc, P.gemv_bulk_grid, mode, cid, st);
+        return;
+    }
     if (mode == 1) {
         if (vec) k_gemv_tiles<true, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
         else k_gemv_tiles<false, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
@@ -145,6 +149,185 @@ int gemv_max_grid() {
     if (occ < 1) occ = 1;
     int g = sms * occ;
     return g > kMaxPartials ? kMaxPartials : g;
+}
+
+// --------------------------------------------------------- GEMV, TMA-bulk pipelined variant
+// Warp-specialised persistent kernel, one CTA per SM: warp 8 (one elected lane) is the
+// producer and streams each tile — kBulkRB rows x kGemvCW columns of H plus the matching
+// kGemvCW chunk of the vector — into a kBulkStages-deep shared-memory ring with 1-D
+// cp.async.bulk copies (SASS UBLKCP) completing on an mbarrier (transaction bytes); H uses an
+// L2 evict-first cache policy.  Warps 0-7 each reduce one row of the tile from shared memory
+// and release the stage.  Tiles are assigned to CTAs as contiguous ranges in column-block-
+// major order (balanced to one tile, consecutive tiles share the vector chunk).  Output
+// (ypart[row][cb], p^T H p) is identical in layout to k_gemv_tiles.
+constexpr int kBulkRB = 8;
+constexpr int kBulkStages = 3;
+constexpr int kBulkConsumers = 8;
+constexpr int kBulkThreads = 32 * (kBulkConsumers + 1);
+constexpr int kBulkStageDoubles = kBulkRB * kGemvCW + kGemvCW;
+constexpr size_t kBulkSmem = (size_t)kBulkStages * kBulkStageDoubles * 8 + 2 * kBulkStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *ptr) {
+    return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+k_gemv_bulk(const double *__restrict__ H, int64_t ldh, int nrows, int ncols, const double *__restrict__ p,
+            const double *__restrict__ pdot, double *__restrict__ ypart, int ncb, double *__restrict__ dpart,
+            Scalars *sc, int cid) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[kBulkThreads / 32];
+    if (MODE == 1 && sc->done) return;
+    double *stages = reinterpret_cast<double *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kBulkStages * kBulkStageDoubles * 8);
+    uint64_t *empty = full + kBulkStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kBulkStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kBulkConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int nrb = (nrows + kBulkRB - 1) / kBulkRB;
+    const int64_t ntiles = (int64_t)nrb * ncb;
+    const int64_t t0 = ntiles * blockIdx.x / gridDim.x;
+    const int64_t t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+    double dacc = 0.0;
+    if (warp == kBulkConsumers) {
+        if (lane == 0) {
+            uint64_t pol_h, pol_p;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_h));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_p));
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = t0; t < t1; ++t) {
+                const int cb = (int)(t / nrb), rb = (int)(t % nrb);
+                const int c0 = cb * kGemvCW;
+                const int cw = min(kGemvCW, ncols - c0);
+                const int cwb = (cw + 1) & ~1;             // 16-byte multiple (reads ldh padding)
+                const int rows = min(kBulkRB, nrows - rb * kBulkRB);
+                mbar_wait(&empty[stage], phase ^ 1u);
+                double *sH = stages + (size_t)stage * kBulkStageDoubles;
+                double *sp = sH + kBulkRB * kGemvCW;
+                mbar_expect_tx(&full[stage], (uint32_t)((rows + 1) * cwb * 8));
+                for (int r = 0; r < rows; ++r)
+                    bulk_g2s(sH + r * kGemvCW, H + (int64_t)(rb * kBulkRB + r) * ldh + c0, (uint32_t)(cwb * 8),
+                             &full[stage], pol_h);
+                bulk_g2s(sp, p + c0, (uint32_t)(cwb * 8), &full[stage], pol_p);
+                if (++stage == kBulkStages) { stage = 0; phase ^= 1u; }
+            }
+        }
+        __syncwarp();
+    } else {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            const int cb = (int)(t / nrb), rb = (int)(t % nrb);
+            const int c0 = cb * kGemvCW;
+            const int cw = min(kGemvCW, ncols - c0);
+            const int rows = min(kBulkRB, nrows - rb * kBulkRB);
+            mbar_wait(&full[stage], phase);
+            if (warp < rows) {
+                const double *sH = stages + (size_t)stage * kBulkStageDoubles + warp * kGemvCW;
+                const double *sp = stages + (size_t)stage * kBulkStageDoubles + kBulkRB * kGemvCW;
+                const double2 *hv = reinterpret_cast<const double2 *>(sH);
+                const double2 *pv = reinterpret_cast<const double2 *>(sp);
+                const int nv = cw >> 1;
+                double a = 0.0, b = 0.0;
+#pragma unroll 4
+                for (int k = lane; k < nv; k += 32) {
+                    const double2 h = hv[k], q = pv[k];
+                    a = fma(h.x, q.x, a);
+                    b = fma(h.y, q.y, b);
+                }
+                if ((cw & 1) && lane == 0) a = fma(sH[cw - 1], sp[cw - 1], a);
+                const double s = warp_sum(a + b);
+                if (lane == 0) {
+                    const int row = rb * kBulkRB + warp;
+                    ypart[(int64_t)row * ncb + cb] = s;
+                    if (pdot) dacc = fma(pdot[row], s, dacc);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == kBulkStages) { stage = 0; phase ^= 1u; }
+        }
+    }
+    if (pdot == nullptr) return;
+    const double bs = block_sum(dacc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
+    if (last_block(&sc->counters[cid])) {
+        const double tot = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[cid] = 0;
+            sc->S_H = tot;
+            if (MODE == 1) {
+                const double pkp = tot + sc->S_b + sc->S_c;
+                sc->pKp = pkp;
+                if (!(pkp > 0.0) || !finite_d(pkp)) {
+                    sc->breakdown = 1;
+                    sc->done = 1;
+                    sc->alpha = 0.0;
+                } else {
+                    sc->alpha = sc->rho / pkp;
+                }
+            }
+        }
+    }
+}
+
+bool gemv_bulk_ok(const Prob &P) {
+    return ((P.ldh & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.H) & 15) == 0);
+}
+
+int gemv_bulk_grid() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_gemv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+        cudaFuncSetAttribute(k_gemv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+    }
+    return sms;
+}
+
+// v must be 16-byte aligned and readable up to round_up(ncols, 2) doubles (workspace vectors).
+void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb, double *dpart,
+                      Scalars *sc, int grid, int mode, int cid, cudaStream_t st) {
+    if (P.n == 0) return;
+    if (mode == 1)
+        k_gemv_bulk<1><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+    else
+        k_gemv_bulk<0><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
 }
 
 // ------------------------------------------------------------------------------ SpMV (A v)

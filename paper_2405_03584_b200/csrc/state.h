@@ -64,6 +64,8 @@ struct Prob {
     const double *ATval;
     const double *g, *l, *u, *xl, *xu;
     double *diagH;
+    int gemv_bulk;         // 1: use the TMA-bulk GEMV (k_gemv_bulk) with grid gemv_bulk_grid
+    int gemv_bulk_grid;
 };
 
 // Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).

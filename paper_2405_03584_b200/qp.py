@@ -144,6 +144,13 @@ class QP:
         L.check(L.ipm_get_trace(self.ctx, recs, cnt.value, C.byref(cnt)), self.ctx)
         return [{k: getattr(r, k) for k, _ in L.ipm_trace_rec._fields_} for r in recs[:cnt.value]]
 
+    def profile(self, what: str = "gemv", reps: int = 20) -> float:
+        """Average device ms per launch of one hot-path stage (CUDA events on our stream)."""
+        code = {"gemv": 0, "spmv": 1, "pcg_iter": 2}[what]
+        ms = C.c_double()
+        L.check(L.ipm_profile(self.ctx, code, int(reps), C.byref(ms)), self.ctx)
+        return ms.value
+
     def kernel_launches(self) -> int:
         return int(L.ipm_kernel_launches(self.ctx))
 

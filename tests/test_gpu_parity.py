@@ -62,6 +62,27 @@ def test_op_apply_bit_exact_on_dyadic_inputs():
     assert np.array_equal(y, yref)
 
 
+@pytest.mark.parametrize("n", [777, 2048, 3071])
+def test_gemv_kernels_agree_bitwise(n):
+    """LDG-tile and TMA-bulk GEMV variants accumulate every (row, column block) partial in
+    the same lane order, so K v is bit-identical between them."""
+    q = planted_qp(n, 200, density=0.02, rank=32, seed=n, rows="mixed")
+    a = _qp(q, gemv_kernel=1)
+    b = _qp(q, gemv_kernel=2)
+    sb, sc, v = _rand_sigmas(q, 3)
+    ya = a.op_apply(sb, sc, v)
+    yb = b.op_apply(sb, sc, v)
+    assert torch.equal(ya, yb)
+    yref = okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v, dtype=np.longdouble).astype(np.float64)
+    assert np.linalg.norm(yb.cpu().numpy() - yref) <= 1e-12 * np.linalg.norm(yref)
+
+
+@pytest.mark.parametrize("gk", [1, 2])
+def test_ipm_both_gemv_kernels(gk):
+    q = planted_qp(1500, 300, density=0.02, rank=32, seed=11, rows="vmat", var="box")
+    _check_against_oracle(q, dict(gemv_kernel=gk))
+
+
 def test_device_hessian_bitwise_equals_numpy():
     q = planted_qp(777, 0, rank=64, seed=4)
     H, ldh = device_hessian(q, DEV)

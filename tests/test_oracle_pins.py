@@ -147,6 +147,7 @@ def test_condensed_matrix_is_schur_complement():
     it = _random_interior_iterate(p, 3)
     r = residuals(p, it)
     Q, B, D, _, _ = reduced_system(p, it, r)
+    B = B.toarray()
     K1 = Q + B.T @ (B / D[:, None])
     sig_b = np.zeros(p.n)
     sig_b[p.J_l] += it.lam["lx"] / it.s["lx"]
@@ -154,13 +155,13 @@ def test_condensed_matrix_is_schur_complement():
     sig_c = np.zeros(p.m)
     sig_c[p.I_l] += it.lam["lA"] / it.s["lA"]
     sig_c[p.I_u] += it.lam["uA"] / it.s["uA"]
-    K2 = okkt.condensed_matrix(p.H, p.A, sig_b, sig_c)
+    K2 = okkt.condensed_matrix(p.H, p.A_dense(), sig_b, sig_c)
     assert np.max(np.abs(K1 - K2)) <= 1e-13 * np.max(np.abs(K1))
     # diag identity e_j^T K e_j and the colsq formula
-    dj = okkt.jacobi_diag(p.H, p.A, sig_b, sig_c)
+    dj = okkt.jacobi_diag(p.H, p.A_dense(), sig_b, sig_c)
     assert np.max(np.abs(dj - np.diag(K1))) <= 1e-13 * np.max(np.abs(dj))
     v = np.random.default_rng(0).normal(size=p.n)
-    assert np.max(np.abs(okkt.condensed_apply(p.H, p.A, sig_b, sig_c, v) - K1 @ v)) <= 1e-12 * np.max(np.abs(K1 @ v))
+    assert np.max(np.abs(okkt.condensed_apply(p.H, p.A_dense(), sig_b, sig_c, v) - K1 @ v)) <= 1e-12 * np.max(np.abs(K1 @ v))
 
 
 # ---------------------------------------------------------------- whole-IPM pins
@@ -178,7 +179,7 @@ def test_ipm_matches_active_set_bruteforce(block):
     for seed in range(25 * block, 25 * block + 25):
         q = _active_set_case(seed)
         p = Problem.from_data(q)
-        best = solve_active_set(p.H, p.g, p.A, p.l, p.u, p.xl, p.xu)
+        best = solve_active_set(p.H, p.g, p.A_dense(), p.l, p.u, p.xl, p.xu)
         assert best is not None, seed
         res = solve(p)
         assert res.status == "converged", seed
@@ -237,7 +238,7 @@ def test_ipm_invariants_and_certificate():
         assert np.all(res.it.s[f] > 0) and np.all(res.it.lam[f] > 0)
     assert res.it.mu <= opt.mu_tol and res.trace[-1]["kkt"] < res.it.mu
     lam = full_multipliers(p, res.it)
-    cert = okkt.kkt_certificate(p.H, p.g, p.A, p.l, p.u, p.xl, p.xu, res.x, lam["lA"], lam["uA"], lam["lx"], lam["ux"])
+    cert = okkt.kkt_certificate(p.H, p.g, p.A_dense(), p.l, p.u, p.xl, p.xu, res.x, lam["lA"], lam["uA"], lam["lx"], lam["ux"])
     assert cert["stationarity"] < 1e-7 and cert["infeasibility"] < 1e-7
     assert cert["min_multiplier"] == 0.0 and cert["complementarity"] < 1e-7
 
@@ -256,7 +257,7 @@ def test_mehrotra_matches_active_set():
     for seed in range(20):
         q = _active_set_case(500 + seed)
         p = Problem.from_data(q)
-        best = solve_active_set(p.H, p.g, p.A, p.l, p.u, p.xl, p.xu)
+        best = solve_active_set(p.H, p.g, p.A_dense(), p.l, p.u, p.xl, p.xu)
         res = solve(p, Options(predictor_corrector=True))
         assert res.status == "converged", seed
         assert np.max(np.abs(res.x - best[0])) <= 1e-5, seed
