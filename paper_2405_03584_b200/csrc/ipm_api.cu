@@ -43,6 +43,21 @@ bool dbg() {
             fflush(stderr);                       \
         }                                         \
     } while (0)
+// IPM_DEBUG=2: synchronise after each stage and report (localises hangs / faults).
+static int dbg_level() {
+    const char *e = getenv("IPM_DEBUG");
+    return e ? atoi(e) : 0;
+}
+#define DSYNC(label)                                                                        \
+    do {                                                                                    \
+        if (dbg_level() >= 2) {                                                             \
+            fprintf(stderr, "[ipm] >> %s\n", label);                                        \
+            fflush(stderr);                                                                 \
+            cudaError_t e2_ = cudaStreamSynchronize(ctx->st);                               \
+            fprintf(stderr, "[ipm] << %s: %s\n", label, cudaGetErrorString(e2_));           \
+            fflush(stderr);                                                                 \
+        }                                                                                   \
+    } while (0)
 
 struct Layout {
     size_t total = 0;
@@ -254,6 +269,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
     Vecs &V = ctx->V;
     int64_t maxit = ctx->opt.pcg_max_iter > 0 ? ctx->opt.pcg_max_iter : 10 * (int64_t)ctx->n;
     launch_pcg_init(P, V, ctx->sc, V.rhs, V.dx, rtol, ctx->opt.pcg_atol, maxit, ctx->st);
+    DSYNC("pcg_init");
     ctx->launches += 1;
     CKL();
     if (ctx->opt.use_graph) TRY(build_graph(ctx));
@@ -309,8 +325,11 @@ ipm_status residuals(ipm_ctx *ctx, double mu) {
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
     launch_gemv(P, V.x, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+    DSYNC("gemv Hx");
     launch_spmv(P, V.x, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
+    DSYNC("spmv Ax");
     launch_residuals(P, V, ctx->G, ctx->sc, mu, ctx->st);
+    DSYNC("residual kernels");
     ctx->launches += 2 + 2 * (P.m > 0 ? 1 : 0);
     CKL();
     return IPM_OK;
@@ -349,8 +368,11 @@ ipm_status start_point(ipm_ctx *ctx) {
     const int warm = ctx->warm_pending ? 1 : 0;
     ctx->warm_pending = false;
     launch_init_x(P, V, warm, ctx->opt.warm_shift, ctx->st);
+    DSYNC("init_x");
     launch_spmv(P, V.x, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
+    DSYNC("spmv Ax0");
     launch_init_slacks(P, V, ctx->sc, warm, ctx->opt.warm_shift, ctx->st);
+    DSYNC("init_slacks");
     ctx->launches += 2 + 2 * (P.m > 0 ? 1 : 0);
     TRY(sync_scalars(ctx));
     if (ctx->nbounds == 0) ctx->mu = ctx->opt.mu_tol;                                   // R13
@@ -363,8 +385,11 @@ ipm_status solve_impl(ipm_ctx *ctx) {
     ctx->trace.clear();
     ipm_stats &S = ctx->stats;
     S = ipm_stats{};
+    DSYNC("solve entry");
     CK(cudaMemsetAsync(&ctx->sc->nonfinite, 0, sizeof(int64_t), ctx->st));
+    DSYNC("memset");
     CK(cudaEventRecord(ctx->ev[0], ctx->st));
+    DSYNC("event");
     TRY(start_point(ctx));
     ctx->have_iterate = true;
     TRY(residuals(ctx, ctx->mu));

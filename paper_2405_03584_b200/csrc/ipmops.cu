@@ -219,7 +219,10 @@ k_resid_n(int n, int ncb, const double *__restrict__ ypart, const int64_t *__res
     const int gpb = blockDim.x / G;
     double rhm = 0.0, prim = 0.0, comp = 0.0, lsm = 0.0, obj = 0.0;
     int bad = 0;
-    for (int j = blockIdx.x * gpb + threadIdx.x / G; j < n; j += gridDim.x * gpb) {
+    // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int j = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double hs = 0.0, at = 0.0;
         for (int c = gl; c < ncb; c += G) hs += ypart[(int64_t)j * ncb + c];
         if (lamd != nullptr) {
@@ -228,7 +231,7 @@ k_resid_n(int n, int ncb, const double *__restrict__ ypart, const int64_t *__res
         }
         hs = group_sum<G>(hs);
         at = group_sum<G>(at);
-        if (gl == 0) {
+        if (act && gl == 0) {
             const double xj = x[j];
             Hx[j] = hs;
             const double rh = hs + g[j] - at - lam_l[j] + lam_u[j];
@@ -335,7 +338,10 @@ k_sigma_n_jacobi(int n, const double *__restrict__ xl, const double *__restrict_
                  double *__restrict__ Minv) {
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
-    for (int j = blockIdx.x * gpb + threadIdx.x / G; j < n; j += gridDim.x * gpb) {
+    // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int j = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double s = 0.0;
         if (sigc != nullptr) {
             const int64_t e = ATrp[j + 1];
@@ -345,7 +351,7 @@ k_sigma_n_jacobi(int n, const double *__restrict__ xl, const double *__restrict_
             }
         }
         s = group_sum<G>(s);
-        if (gl == 0) {
+        if (act && gl == 0) {
             double sb = 0.0;
             if (has(xl[j])) sb += lam_l[j] / s_l[j];
             if (has(xu[j])) sb += lam_u[j] / s_u[j];
@@ -414,14 +420,17 @@ k_rhs_n(int n, const double *__restrict__ xl, const double *__restrict__ xu, con
         const double *__restrict__ w, double *__restrict__ rhs, double mu, int mode, double smu) {
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
-    for (int j = blockIdx.x * gpb + threadIdx.x / G; j < n; j += gridDim.x * gpb) {
+    // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int j = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double at = 0.0;
         if (w != nullptr) {
             const int64_t e = ATrp[j + 1];
             for (int64_t k = ATrp[j] + gl; k < e; k += G) at = fma(__ldg(ATval + k), __ldg(w + __ldg(ATcol + k)), at);
         }
         at = group_sum<G>(at);
-        if (gl == 0) {
+        if (act && gl == 0) {
             double r1 = -rH[j];
             double ca = 0.0, cb = 0.0;
             if (has(xl[j])) {

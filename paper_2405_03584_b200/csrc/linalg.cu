@@ -399,7 +399,10 @@ k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *_
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
     double acc = 0.0;
-    for (int i = blockIdx.x * gpb + threadIdx.x / G; i < n; i += gridDim.x * gpb) {
+    // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double s = 0.0;
         for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
         if (MODE != 2 && t != nullptr) {
@@ -407,7 +410,7 @@ k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *_
             for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
         }
         s = group_sum<G>(s);
-        if (gl == 0) {
+        if (act && gl == 0) {
             const double yi = (MODE == 2) ? s : fma(sigb[i], v[i], s);
             if (MODE == 1) {
                 const double ri = rhs[i] - yi;
@@ -462,7 +465,10 @@ k_jacobi(int n, const double *__restrict__ diagH, const double *__restrict__ sig
          const double *__restrict__ sigc, double *__restrict__ out, int invert) {
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
-    for (int i = blockIdx.x * gpb + threadIdx.x / G; i < n; i += gridDim.x * gpb) {
+    // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double s = 0.0;
         if (sigc != nullptr) {
             const int64_t e = ATrp[i + 1];
@@ -472,7 +478,7 @@ k_jacobi(int n, const double *__restrict__ diagH, const double *__restrict__ sig
             }
         }
         s = group_sum<G>(s);
-        if (gl == 0) {
+        if (act && gl == 0) {
             const double d = diagH[i] + sigb[i] + s;
             out[i] = invert ? 1.0 / d : d;
         }

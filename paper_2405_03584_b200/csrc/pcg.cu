@@ -15,7 +15,24 @@
 #include "kernels.h"
 #include "state.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace ipm {
+
+static void dstage(const char *what, cudaStream_t st) {
+    static int lvl = -1;
+    if (lvl < 0) {
+        const char *e = getenv("IPM_DEBUG");
+        lvl = e ? atoi(e) : 0;
+    }
+    if (lvl < 3) return;
+    fprintf(stderr, "[ipm-pcg] >> %s\n", what);
+    fflush(stderr);
+    cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[ipm-pcg] << %s %s\n", what, cudaGetErrorString(e));
+    fflush(stderr);
+}
 
 static int grid_for(int64_t units, int per_block) {
     int64_t g = (units + per_block - 1) / per_block;
@@ -173,7 +190,10 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
     double rz = 0.0, rr = 0.0;
-    for (int i = blockIdx.x * gpb + threadIdx.x / G; i < n; i += gridDim.x * gpb) {
+    // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double s = 0.0;
         for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
         if (t != nullptr) {
@@ -181,7 +201,7 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
             for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
         }
         s = group_sum<G>(s);
-        if (gl == 0) {
+        if (act && gl == 0) {
             const double pi = p[i];
             const double yi = fma(sigb[i], pi, s);
             x[i] = fma(alpha, pi, x[i]);
@@ -222,8 +242,11 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
                           cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
     const int grid = grid_for(P.n, kBlock);
     k_pcg_p<<<grid, kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2], sc);
+    if (!use_cond) dstage("pcg_p", st);
     launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
+    if (!use_cond) dstage("spmv", st);
     launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);
+    if (!use_cond) dstage("gemv", st);
     const int ug = grid_for(P.n, kBlock / G);
     const double *t = (P.m > 0) ? V.pt : nullptr;
 #define IPM_UPD(GG)                                                                                              \

@@ -1,8 +1,9 @@
-"""Bounded GPU diagnostic: create + solve C1 with the host-loop PCG and the graph PCG."""
+"""Bounded GPU diagnostic: stage by stage on C1 (IPM_DEBUG=2 syncs after every stage)."""
 import faulthandler, os, sys, time
-faulthandler.dump_traceback_later(100, exit=True)
+faulthandler.dump_traceback_later(40, exit=True)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("IPM_DEBUG", "1")
+os.environ.setdefault("IPM_DEBUG", "2")
+import numpy as np
 import torch
 print("torch", torch.__version__, torch.cuda.get_device_name(0), flush=True)
 from gen.planted import config
@@ -10,8 +11,11 @@ from gen.torch_io import problem_tensors
 from paper_2405_03584_b200 import QP
 q = config("C1", 0)
 t = problem_tensors(q, torch.device("cuda", 0))
-for ug in [int(a) for a in sys.argv[1:]] or [0, 1]:
-    t0 = time.time()
-    qp = QP(device="cuda:0", use_graph=ug, **t)
-    print("created", ug, time.time() - t0, flush=True)
-    print("status", qp.solve(), qp.stats(), time.time() - t0, flush=True)
+ug = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+gk = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+qp = QP(device="cuda:0", use_graph=ug, gemv_kernel=gk, **t)
+print("created", flush=True)
+sb = np.ones(q.n); sc = np.ones(q.m); v = np.ones(q.n)
+y = qp.op_apply(sb, sc, v); torch.cuda.synchronize(); print("op_apply ok", float(y.sum()), flush=True)
+x, it = qp.pcg(sb, sc, v, 1e-10); print("pcg ok", it, flush=True)
+print("status", qp.solve(), qp.stats(), flush=True)
