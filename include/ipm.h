@@ -96,10 +96,21 @@ typedef struct {
     const double *A_val;        /* nnz, BORROWED; finite */
     const double *l, *u;        /* m each, copied; -INF / +INF = absent; l < u where both finite */
     const double *xl, *xu;      /* n each, copied; xl < xu where both finite */
-    int64_t row_begin, row_end; /* row block of H (and of all x-space vectors) owned by this rank */
-    int32_t rank, nranks;       /* nranks == 1 => unsharded (row_begin=0,row_end=n) */
-    const void *nccl_unique_id_host; /* HOST pointer to an ncclUniqueId (128 bytes), nranks > 1 */
+    /* Row sharding.  With chunk = ceil(n / nranks), rank r must own rows
+     * [r*chunk, min(n, (r+1)*chunk)) of H and the same slice of every x-space vector; A (and
+     * all m-space vectors) are replicated on every rank.  g, xl, xu are passed FULL length
+     * (each rank copies its slice).  comm_kind: 0 = none (nranks must be 1); 1 = NCCL,
+     * comm_handle_host -> ncclUniqueId (128 bytes, from ipm_nccl_unique_id on rank 0,
+     * broadcast by the caller); 2 = in-process group, comm_handle_host = ipm_group* (one host
+     * thread per rank must drive its context).  comm_kind 2 with nranks 1 runs the sharded
+     * code path on one context (testing). */
+    int64_t row_begin, row_end;
+    int32_t rank, nranks;
+    int32_t comm_kind;
+    const void *comm_handle_host;
 } ipm_problem;
+
+typedef struct ipm_group ipm_group;  /* in-process rank group (comm_kind 2) */
 
 typedef struct {
     int32_t status;             /* final ipm_status of the last ipm_solve */
@@ -128,6 +139,13 @@ typedef struct {
 /* Fill defaults (documented per field above). */
 void ipm_options_default(ipm_options *opt);
 
+/* Sharding helpers.  ipm_nccl_unique_id writes an ncclUniqueId (needs >= 128 bytes) for
+ * rank 0 to broadcast; ipm_group_create/destroy manage an in-process group of nranks
+ * contexts (destroy only after every member context is destroyed). */
+ipm_status ipm_nccl_unique_id(void *id_out_host, size_t bytes);
+ipm_status ipm_group_create(int32_t nranks, ipm_group **group);
+void ipm_group_destroy(ipm_group *group);
+
 /* Bytes of device workspace ipm_create needs for this problem (host-only arithmetic). */
 ipm_status ipm_workspace_size(const ipm_problem *prob, const ipm_options *opt, size_t *bytes);
 
@@ -145,7 +163,8 @@ ipm_status ipm_create(ipm_ctx **ctx, const ipm_problem *prob, const ipm_options 
  * ipm_warm_start was called since the last solve. */
 ipm_status ipm_solve(ipm_ctx *ctx);
 
-/* Copy the current iterate out (device pointers; NULL = skip).  obj_host: host double. */
+/* Copy the current iterate out (device pointers; NULL = skip).  obj_host: host double.
+ * Sharded: x, lam_lx, lam_ux are this rank's row slice; lam_lA, lam_uA are full (replicated). */
 ipm_status ipm_get_solution(ipm_ctx *ctx, double *x, double *lam_lA, double *lam_uA,
                             double *lam_lx, double *lam_ux, double *obj_host);
 
@@ -172,7 +191,9 @@ ipm_status ipm_get_iterate(ipm_ctx *ctx, double *x, double *const s4[4], double 
  *   ipm_op_apply: y = K v with K of (1), Sigma_b = sig_b (n), Sigma_c = sig_c (m)
  *   ipm_op_diag : d = diag(K) = diag(H) + sig_b + colsq(A, sig_c)
  *   ipm_pcg     : Jacobi-PCG on K x = rhs from x = 0 to ||r|| <= rtol ||rhs|| (true residual
- *                 confirmed); iters_host gets the iteration count. */
+ *                 confirmed); iters_host gets the iteration count.
+ * Sharded contexts: v is FULL length (n); sig_b, d, y, rhs and x are this rank's row slice;
+ * sig_c is full (m). */
 ipm_status ipm_op_apply(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *v,
                         double *y);
 ipm_status ipm_op_diag(ipm_ctx *ctx, const double *sig_b, const double *sig_c, double *d);

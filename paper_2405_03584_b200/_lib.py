@@ -38,7 +38,7 @@ class ipm_problem(C.Structure):
                 ("g", C.c_void_p), ("A_rowptr", C.c_void_p), ("A_col", C.c_void_p), ("A_val", C.c_void_p),
                 ("l", C.c_void_p), ("u", C.c_void_p), ("xl", C.c_void_p), ("xu", C.c_void_p),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("nccl_unique_id_host", C.c_void_p)]
+                ("comm_kind", C.c_int32), ("comm_handle_host", C.c_void_p)]
 
 
 class ipm_stats(C.Structure):
@@ -60,6 +60,9 @@ _S = C.c_int32
 _sigs = {
     "ipm_abi_version": ([], C.c_int32),
     "ipm_options_default": ([C.POINTER(ipm_options)], None),
+    "ipm_nccl_unique_id": ([_P, C.c_size_t], _S),
+    "ipm_group_create": ([C.c_int32, C.POINTER(_P)], _S),
+    "ipm_group_destroy": ([_P], None),
     "ipm_workspace_size": ([C.POINTER(ipm_problem), C.POINTER(ipm_options), C.POINTER(C.c_size_t)], _S),
     "ipm_create": ([C.POINTER(_P), C.POINTER(ipm_problem), C.POINTER(ipm_options), _P, C.c_size_t, _P], _S),
     "ipm_solve": ([_P], _S),

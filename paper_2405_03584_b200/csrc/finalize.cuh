@@ -1,0 +1,84 @@
+// finalize.cuh — the scalar "epilogues" of the reductions, shared by the kernels' last
+// blocks (one GPU) and by k_xcombine (row-sharded: applied to the rank-ordered combination
+// of every rank's partials, so all ranks take bit-identical decisions).
+#pragma once
+
+#include "common.cuh"
+#include "state.h"
+
+namespace ipm {
+
+// PCG start (S:225 stopping rule ||r||_2 <= max(rtol ||rhs||_2, atol)).
+__device__ __forceinline__ void fin_pcg_init(Scalars *sc, double trz, double trr, double rtol, double atol,
+                                             int64_t maxit) {
+    sc->rho = trz;
+    sc->rho_old = trz;
+    sc->rr = trr;
+    sc->rhs2 = trr;
+    const double t1 = rtol * rtol * trr, t2 = atol * atol;
+    sc->tol2 = t1 > t2 ? t1 : t2;
+    sc->it = 0;
+    sc->it_rs = 0;
+    sc->maxit = maxit;
+    sc->breakdown = 0;
+    sc->S_b = sc->S_c = sc->S_H = 0.0;
+    sc->done = (trr <= sc->tol2) ? 1 : 0;
+    if (!finite_d(trr) || !finite_d(trz)) {
+        sc->done = 1;
+        sc->breakdown = 1;
+    }
+}
+
+__device__ __forceinline__ void fin_pcg_restart(Scalars *sc, double trz, double trr) {
+    sc->rho = trz;
+    sc->rho_old = trz;
+    sc->rr = trr;
+    sc->it_rs = 0;
+    sc->done = (trr <= sc->tol2 || sc->it >= sc->maxit) ? 1 : 0;
+}
+
+// alpha = rho / p^T K p; p^T K p <= 0 is a breakdown.
+__device__ __forceinline__ void fin_pcg_alpha(Scalars *sc, double pkp) {
+    sc->pKp = pkp;
+    if (!(pkp > 0.0) || !finite_d(pkp)) {
+        sc->breakdown = 1;
+        sc->done = 1;
+        sc->alpha = 0.0;
+    } else {
+        sc->alpha = sc->rho / pkp;
+    }
+}
+
+// end of a PCG iteration: rho, ||r||^2, iteration count and the stop decision.
+__device__ __forceinline__ int fin_pcg_update(Scalars *sc, double trz, double trr) {
+    sc->rho_old = sc->rho;
+    sc->rho = trz;
+    sc->rr = trr;
+    sc->it += 1;
+    sc->it_rs += 1;
+    int stop = 0;
+    if (trr <= sc->tol2 || sc->it >= sc->maxit) stop = 1;
+    if (!finite_d(trr) || !finite_d(trz)) {
+        stop = 1;
+        sc->breakdown = 1;
+    }
+    sc->done = stop;
+    return stop;
+}
+
+// fraction to the boundary: alpha = min(1, tau * min ratio); empty set -> 1.
+__device__ __forceinline__ void fin_recover(Scalars *sc, double minx, double minl, double tau) {
+    sc->alpha_x = fmin(1.0, tau * fmin(minx, sc->minx_m));
+    sc->alpha_l = fmin(1.0, tau * fmin(minl, sc->minl_m));
+}
+
+__device__ __forceinline__ void fin_resid(Scalars *sc, double rh, double prim, double comp, double lsm, double obj) {
+    sc->rH_max = rh;
+    sc->prim_max = fmax(prim, sc->prim_max_m);
+    sc->comp_max = fmax(comp, sc->comp_max_m);
+    sc->ls_max = fmax(lsm, sc->ls_max_m);
+    sc->obj = obj;
+    if (!finite_d(obj)) sc->nonfinite = 1;
+}
+
+}  // namespace ipm

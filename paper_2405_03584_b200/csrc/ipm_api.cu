@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/ipm.h"
+#include "comm.h"
 #include "kernels.h"
 #include "state.h"
 
@@ -72,7 +73,7 @@ struct Offsets {
     size_t sc;
     size_t nvec[40];
     size_t mvec[40];
-    size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad;
+    size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad, gfull, xloc_all;
     int n_nvec, n_mvec;
     int nchunk;
 };
@@ -80,10 +81,13 @@ struct Offsets {
 constexpr int kNVec = 30;   // n-space vectors in Vecs (see assign_vectors)
 constexpr int kMVec = 24;   // m-space vectors
 
-Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, Layout &L) {
+// nloc = rows owned by this rank; every n-space vector gets chunk = ceil(n/P) (+2 pad) slots
+// so the allgather can send equal blocks and the bulk GEMV may read one padding element.
+Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks, Layout &L) {
     Offsets o{};
+    const int64_t chunk = (ncols + nranks - 1) / nranks;
     o.sc = L.take(sizeof(Scalars));
-    for (int i = 0; i < kNVec; ++i) o.nvec[i] = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+    for (int i = 0; i < kNVec; ++i) o.nvec[i] = L.take(sizeof(double) * (std::max<int64_t>(chunk, 1) + 2));
     for (int i = 0; i < kMVec; ++i) o.mvec[i] = L.take(sizeof(double) * std::max<int64_t>(m, 1));
     o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) * gemv_ncb((int)ncols));
     o.part = L.take(sizeof(double) * kMaxPartials * 8);
@@ -99,6 +103,8 @@ Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, Layout &L)
     o.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(128, m));
     o.cnt = L.take(sizeof(int) * (size_t)o.nchunk * std::max<int64_t>(nloc, 1));
     o.bad = L.take(sizeof(unsigned long long));
+    o.gfull = L.take(sizeof(double) * ((size_t)chunk * nranks + 2));
+    o.xloc_all = L.take(sizeof(double) * 8 * (size_t)nranks);
     return o;
 }
 
@@ -135,6 +141,10 @@ struct ipm_ctx {
     std::string err;
     int64_t launches = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // row-sharded mode
+    ipm::Comm *comm = nullptr;
+    bool sharded = false;
+    int64_t chunk = 0;
 };
 
 namespace {
@@ -200,6 +210,35 @@ void assign_vectors(ipm_ctx *c, const Offsets &o) {
     V.lamd = mv[j++]; V.pt = mv[j++];
     V.ypart = reinterpret_cast<double *>(b + o.ypart);
     for (int i = 0; i < 8; ++i) V.part[i] = reinterpret_cast<double *>(b + o.part) + (size_t)i * kMaxPartials;
+    V.gfull = reinterpret_cast<double *>(b + o.gfull);
+    V.xloc_all = reinterpret_cast<double *>(b + o.xloc_all);
+}
+
+// ------------------------------------------------------------------- sharded collectives
+// Full-length copy of an x-space vector: the vector itself on one GPU, else an allgather of
+// every rank's chunk into V.gfull (rank r's rows land at [r*chunk, ...), i.e. global order).
+ipm_status gather(ipm_ctx *ctx, const double *local, const double **full) {
+    if (!ctx->sharded) {
+        *full = local;
+        return IPM_OK;
+    }
+    std::string e;
+    if (ctx->comm->allgather(local, ctx->V.gfull, sizeof(double) * ctx->chunk, ctx->st, e))
+        return fail(ctx, IPM_ERR_NCCL, "%s", e.c_str());
+    *full = ctx->V.gfull;
+    return IPM_OK;
+}
+
+// Combine this stage's per-rank partials (Scalars::loc) across ranks (shard.cu).
+ipm_status xcombine(ipm_ctx *ctx, int stage, double p0 = 0.0, double p1 = 0.0, int64_t p2 = 0) {
+    if (!ctx->sharded) return IPM_OK;
+    std::string e;
+    if (ctx->comm->allgather(ctx->sc->loc, ctx->V.xloc_all, sizeof(double) * 8, ctx->st, e))
+        return fail(ctx, IPM_ERR_NCCL, "%s", e.c_str());
+    launch_xcombine(ctx->sc, ctx->V.xloc_all, ctx->comm->nranks, stage, p0, p1, p2, ctx->st);
+    ctx->launches += 1;
+    CKL();
+    return IPM_OK;
 }
 
 int choose_group(int64_t nnz_loc, int64_t nloc, int ncb) {
@@ -218,19 +257,36 @@ double pcg_rtol(const ipm_options &o, double mu) {
 
 // ---------------------------------------------------------------------------- operators
 // y = K v with the current sig_b/sig_c (t and ypart are scratch).  mode 1: r = rhs - K v.
-ipm_status op_apply(ipm_ctx *ctx, const double *v_in, double *out, const double *rhs, int mode) {
+// v_local: workspace x-space vector (this rank's rows); v_full: its full-length version or
+// nullptr to gather it.  Result rows are local.
+ipm_status op_apply(ipm_ctx *ctx, const double *v_local, const double *v_full, double *out, const double *rhs,
+                    int mode) {
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
-    // the operand must live in the workspace (16-B aligned, padded): copy caller vectors
-    const double *v = v_in;
-    if (v_in != V.dx && v_in != V.x && v_in != V.pp) {
-        CK(cudaMemcpyAsync(V.py, v_in, sizeof(double) * P.n, cudaMemcpyDeviceToDevice, ctx->st));
-        v = V.py;
-    }
-    launch_spmv(P, v, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 0, ctx->st);
-    launch_gemv(P, v, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
-    launch_apply_reduce(P, ctx->G, ctx->ncb, V.ypart, V.sig_b, v, V.pt, out, rhs, V.part[5], ctx->sc, mode, ctx->st);
+    if (!v_full) TRY(gather(ctx, v_local, &v_full));
+    launch_spmv(P, v_full, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 0, ctx->st);
+    launch_gemv(P, v_full, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+    launch_apply_reduce(P, ctx->G, ctx->ncb, V.ypart, V.sig_b, v_local, V.pt, out, rhs, V.part[5], ctx->sc, mode,
+                        ctx->st);
     ctx->launches += (P.m > 0 ? 1 : 0) + 2;
+    CKL();
+    if (mode == 1) TRY(xcombine(ctx, X_RES2));
+    return IPM_OK;
+}
+
+// One PCG iteration on a row-sharded context (no graph: collectives between the kernels).
+ipm_status pcg_iteration_sharded(ipm_ctx *ctx) {
+    const Prob &P = ctx->P;
+    const Vecs &V = ctx->V;
+    launch_pcg_p(P, V, ctx->sc, ctx->st);
+    const double *pf = nullptr;
+    TRY(gather(ctx, V.pp, &pf));
+    launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
+    launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, ctx->st);
+    TRY(xcombine(ctx, X_PCG_ALPHA));
+    launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, ctx->st);
+    TRY(xcombine(ctx, X_PCG_UPDATE));
+    ctx->launches += 3 + (P.m > 0 ? 1 : 0);
     CKL();
     return IPM_OK;
 }
@@ -272,13 +328,23 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
     DSYNC("pcg_init");
     ctx->launches += 1;
     CKL();
-    if (ctx->opt.use_graph) TRY(build_graph(ctx));
+    TRY(xcombine(ctx, X_PCG_INIT, rtol, ctx->opt.pcg_atol, maxit));
+    const bool graph = ctx->opt.use_graph && !ctx->sharded;
+    if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
     int64_t it_prev = 0;
     for (int round = 0;; ++round) {
-        if (ctx->opt.use_graph) {
+        if (graph) {
             CK(cudaGraphLaunch(ctx->gexec, ctx->st));
             TRY(sync_scalars(ctx));
+        } else if (ctx->sharded) {
+            // host-driven batches; every rank sees the same combined `done`, so all ranks run
+            // the same number of iterations and collectives
+            for (;;) {
+                for (int b = 0; b < 16; ++b) TRY(pcg_iteration_sharded(ctx));
+                TRY(sync_scalars(ctx));
+                if (ctx->hsc->done) break;
+            }
         } else {
             // host-driven fallback: batches of 16 iterations with device-side early exit
             for (;;) {
@@ -293,7 +359,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
         const Scalars &h = *ctx->hsc;
         DBG("pcg round %d: it=%lld rr=%.3e tol2=%.3e done=%lld breakdown=%lld rho=%.3e pKp=%.3e\n", round,
             (long long)h.it, h.rr, h.tol2, (long long)h.done, (long long)h.breakdown, h.rho, h.pKp);
-        if (ctx->opt.use_graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * (3 + (P.m > 0 ? 1 : 0));
+        if (graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * (3 + (P.m > 0 ? 1 : 0));
         it_prev = h.it;
         if (h.breakdown) {
             out.iters = h.it;
@@ -301,7 +367,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
                         (long long)h.it, h.pKp);
         }
         // true residual confirmation: r = rhs - K dx
-        TRY(op_apply(ctx, V.dx, V.pr, V.rhs, 1));
+        TRY(op_apply(ctx, V.dx, nullptr, V.pr, V.rhs, 1));
         TRY(sync_scalars(ctx));
         const double res2 = ctx->hsc->res2, tol2 = ctx->hsc->tol2, rhs2 = ctx->hsc->rhs2;
         out.iters = ctx->hsc->it;
@@ -316,6 +382,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
         launch_pcg_restart(P, V, ctx->sc, ctx->st);
         ctx->launches += 1;
         CKL();
+        TRY(xcombine(ctx, X_PCG_RESTART));
     }
     return IPM_OK;
 }
@@ -324,14 +391,17 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
 ipm_status residuals(ipm_ctx *ctx, double mu) {
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
-    launch_gemv(P, V.x, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+    const double *xf = nullptr;
+    TRY(gather(ctx, V.x, &xf));
+    launch_gemv(P, xf, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
     DSYNC("gemv Hx");
-    launch_spmv(P, V.x, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
+    launch_spmv(P, xf, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
     DSYNC("spmv Ax");
     launch_residuals(P, V, ctx->G, ctx->sc, mu, ctx->st);
     DSYNC("residual kernels");
     ctx->launches += 2 + 2 * (P.m > 0 ? 1 : 0);
     CKL();
+    TRY(xcombine(ctx, X_RESID));
     return IPM_OK;
 }
 
@@ -351,10 +421,13 @@ ipm_status direction(ipm_ctx *ctx, double mu, int mode, double smu, double tau, 
     CK(cudaEventSynchronize(ctx->ev[3]));
     CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
     tpcg += ms;
-    launch_spmv(P, V.dx, nullptr, V.Adx, nullptr, ctx->sc, 0, 0, ctx->st);
+    const double *dxf = nullptr;
+    TRY(gather(ctx, V.dx, &dxf));
+    launch_spmv(P, dxf, nullptr, V.Adx, nullptr, ctx->sc, 0, 0, ctx->st);
     launch_recover(P, V, ctx->sc, tau, aff, ctx->st);
     ctx->launches += 1 + 2 * (P.m > 0 ? 1 : 0);
     CKL();
+    TRY(xcombine(ctx, X_RECOVER, tau));
     return IPM_OK;
 }
 
@@ -369,11 +442,14 @@ ipm_status start_point(ipm_ctx *ctx) {
     ctx->warm_pending = false;
     launch_init_x(P, V, warm, ctx->opt.warm_shift, ctx->st);
     DSYNC("init_x");
-    launch_spmv(P, V.x, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
+    const double *xf = nullptr;
+    TRY(gather(ctx, V.x, &xf));
+    launch_spmv(P, xf, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
     DSYNC("spmv Ax0");
     launch_init_slacks(P, V, ctx->sc, warm, ctx->opt.warm_shift, ctx->st);
     DSYNC("init_slacks");
     ctx->launches += 2 + 2 * (P.m > 0 ? 1 : 0);
+    TRY(xcombine(ctx, X_SUMLS));
     TRY(sync_scalars(ctx));
     if (ctx->nbounds == 0) ctx->mu = ctx->opt.mu_tol;                                   // R13
     else ctx->mu = ctx->opt.mu0_scale * ctx->hsc->sum_ls / (double)ctx->nbounds;      // R5
@@ -409,8 +485,10 @@ ipm_status solve_impl(ipm_ctx *ctx) {
         } else {
             // Mehrotra (R18): affine direction, sigma = (mu_aff/mu_cur)^3, corrector
             launch_sum_ls(ctx->P, ctx->V, ctx->sc, ctx->st);
+            TRY(xcombine(ctx, X_SUMLS));
             TRY(direction(ctx, mu, 1, 0.0, 1.0, 1, po, tpcg));
             launch_muaff(ctx->P, ctx->V, ctx->sc, ctx->st);
+            TRY(xcombine(ctx, X_MUAFF));
             ctx->launches += 2 * (1 + (ctx->P.m > 0 ? 1 : 0));
             TRY(sync_scalars(ctx));
             const double nb = (double)ctx->nbounds;
@@ -425,6 +503,7 @@ ipm_status solve_impl(ipm_ctx *ctx) {
         if (pc) {
             launch_sum_ls(ctx->P, ctx->V, ctx->sc, ctx->st);
             ctx->launches += 1 + (ctx->P.m > 0 ? 1 : 0);
+            TRY(xcombine(ctx, X_SUMLS));
         }
         TRY(residuals(ctx, pc ? 0.0 : mu));
         TRY(sync_scalars(ctx));
@@ -548,7 +627,7 @@ IPM_EXPORT void ipm_options_default(ipm_options *o) {
 }
 
 static void local_rows(const ipm_problem *p, int64_t &row0, int64_t &nloc) {
-    if (p->nranks > 1) {
+    if (p->comm_kind != 0) {
         row0 = p->row_begin;
         nloc = p->row_end - p->row_begin;
     } else {
@@ -557,16 +636,60 @@ static void local_rows(const ipm_problem *p, int64_t &row0, int64_t &nloc) {
     }
 }
 
+static int eff_ranks(const ipm_problem *p) { return p->comm_kind != 0 ? std::max(1, p->nranks) : 1; }
+
+// Rows of rank r under the equal-chunk partition (header: chunk = ceil(n / nranks)).
+static ipm_status check_partition(const ipm_problem *p) {
+    if (p->comm_kind == 0) {
+        if (p->nranks > 1) return fail(nullptr, IPM_ERR_INVALID, "nranks > 1 needs comm_kind 1 (NCCL) or 2 (local group)");
+        return IPM_OK;
+    }
+    if (p->comm_kind != 1 && p->comm_kind != 2) return fail(nullptr, IPM_ERR_INVALID, "unknown comm_kind");
+    if (!p->comm_handle_host) return fail(nullptr, IPM_ERR_INVALID, "comm_handle_host is null");
+    const int64_t P = std::max(1, p->nranks);
+    if (p->rank < 0 || p->rank >= P) return fail(nullptr, IPM_ERR_INVALID, "rank out of range");
+    const int64_t chunk = (p->n + P - 1) / P;
+    const int64_t b = std::min<int64_t>(p->n, p->rank * chunk), e = std::min<int64_t>(p->n, (p->rank + 1) * chunk);
+    if (p->row_begin != b || p->row_end != e || b >= e)
+        return fail(nullptr, IPM_ERR_INVALID,
+                    "row block [%lld,%lld) of rank %d must be [%lld,%lld) (chunk = ceil(n/nranks)) and non-empty",
+                    (long long)p->row_begin, (long long)p->row_end, p->rank, (long long)b, (long long)e);
+    return IPM_OK;
+}
+
 IPM_EXPORT ipm_status ipm_workspace_size(const ipm_problem *p, const ipm_options *opt, size_t *bytes) {
     (void)opt;
     if (!p || !bytes) return fail(nullptr, IPM_ERR_INVALID, "null argument");
     if (p->n < 1 || p->m < 0 || p->nnz < 0) return fail(nullptr, IPM_ERR_INVALID, "bad dimensions");
     int64_t row0, nloc;
     local_rows(p, row0, nloc);
+    if (nloc < 1) return fail(nullptr, IPM_ERR_INVALID, "empty row block");
     Layout L;
-    plan(nloc, p->n, p->m, p->nnz, L);   // nnz of the local A^T block <= nnz
+    plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L);   // nnz of the local A^T block <= nnz
     *bytes = L.total;
     return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_nccl_unique_id(void *out, size_t bytes) {
+    if (!out) return fail(nullptr, IPM_ERR_INVALID, "null argument");
+    std::string e;
+    if (ipm::nccl_unique_id(out, bytes, e)) return fail(nullptr, IPM_ERR_NCCL, "%s", e.c_str());
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_group_create(int32_t nranks, ipm_group **g) {
+    if (!g || nranks < 1) return fail(nullptr, IPM_ERR_INVALID, "bad argument");
+    *g = new ipm_group(nranks);
+    return IPM_OK;
+}
+
+IPM_EXPORT void ipm_group_destroy(ipm_group *g) {
+    if (!g) return;
+    for (auto e : g->ready)
+        if (e) cudaEventDestroy(e);
+    for (auto e : g->copied)
+        if (e) cudaEventDestroy(e);
+    delete g;
 }
 
 static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspace, ipm_stream_t stream) {
@@ -616,10 +739,25 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
 
         // --- device state ------------------------------------------------------------
         Layout L;
-        const Offsets o = plan(nloc, p->n, p->m, p->nnz, L);
+        const Offsets o = plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L);
         CK(cudaMemsetAsync(ctx->ws, 0, L.total, ctx->st));
         ctx->sc = reinterpret_cast<Scalars *>(ctx->ws + o.sc);
         assign_vectors(ctx, o);
+        if (p->comm_kind != 0) {
+            std::string e;
+            ctx->comm = (p->comm_kind == 1)
+                            ? ipm::make_nccl_comm(p->comm_handle_host, p->rank, std::max(1, p->nranks), e)
+                            : ipm::make_local_comm(const_cast<ipm_group *>(
+                                                       static_cast<const ipm_group *>(p->comm_handle_host)),
+                                                   p->rank, e);
+            if (!ctx->comm) return fail(ctx, IPM_ERR_NCCL, "communicator: %s", e.c_str());
+            if (ctx->comm->nranks != std::max(1, p->nranks))
+                return fail(ctx, IPM_ERR_INVALID, "group size %d != nranks %d", ctx->comm->nranks, p->nranks);
+            ctx->sharded = true;
+            ctx->chunk = (p->n + ctx->comm->nranks - 1) / ctx->comm->nranks;
+            const int64_t one = 1;
+            CK(cudaMemcpyAsync(&ctx->sc->sharded, &one, sizeof one, cudaMemcpyHostToDevice, ctx->st));
+        }
         Prob &P = ctx->P;
         P.n = (int)nloc;
         P.m = (int)p->m;
@@ -684,11 +822,7 @@ IPM_EXPORT ipm_status ipm_create(ipm_ctx **out, const ipm_problem *p, const ipm_
         return fail(nullptr, IPM_ERR_INVALID, "bad dimensions (n >= 1, m >= 0, nnz >= 0, ldh >= n)");
     if (p->n > INT32_MAX || p->m > INT32_MAX || p->nnz >= INT32_MAX)
         return fail(nullptr, IPM_ERR_INVALID, "dimension exceeds int32 index range");
-    if (p->nranks > 1) {
-        if (p->row_begin < 0 || p->row_end > p->n || p->row_begin >= p->row_end)
-            return fail(nullptr, IPM_ERR_INVALID, "bad row block [row_begin, row_end)");
-        return fail(nullptr, IPM_ERR_INVALID, "row-sharded path (nranks > 1) is not built in this library version");
-    }
+    if (check_partition(p) != IPM_OK) return IPM_ERR_INVALID;
     if (!p->H || !p->g || !p->xl || !p->xu || (p->m > 0 && (!p->l || !p->u || !p->A_rowptr)) ||
         (p->nnz > 0 && (!p->A_col || !p->A_val)))
         return fail(nullptr, IPM_ERR_INVALID, "null data pointer");
@@ -827,7 +961,15 @@ static ipm_status load_sigmas(ipm_ctx *ctx, const double *sig_b, const double *s
 IPM_EXPORT ipm_status ipm_op_apply(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *v, double *y) {
     if (!ctx || !sig_b || !v || !y || (ctx->m > 0 && !sig_c)) return fail(ctx, IPM_ERR_INVALID, "null argument");
     TRY(load_sigmas(ctx, sig_b, sig_c));
-    TRY(op_apply(ctx, v, y, nullptr, 0));
+    // operands must live in the workspace (16-B aligned, padded for the bulk GEMV)
+    const Vecs &V = ctx->V;
+    CK(cudaMemcpyAsync(V.py, v + ctx->row0, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
+    const double *vf = V.py;
+    if (ctx->sharded) {
+        CK(cudaMemcpyAsync(V.gfull, v, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->st));
+        vf = V.gfull;
+    }
+    TRY(op_apply(ctx, V.py, vf, y, nullptr, 0));
     return IPM_OK;
 }
 
@@ -898,5 +1040,6 @@ IPM_EXPORT void ipm_destroy(ipm_ctx *ctx) {
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->hsc) cudaFreeHost(ctx->hsc);
+    delete ctx->comm;
     delete ctx;
 }

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "state.h"
+#include "finalize.cuh"
 
 namespace ipm {
 
@@ -102,7 +103,7 @@ k_init_slacks(int len, const double *__restrict__ lo, const double *__restrict__
         const double t = sum_partials(dpart, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
-            if (final_) sc->sum_ls = sc->sum_ls_m + t;
+            if (final_) { sc->sum_ls = sc->sum_ls_m + t; sc->loc[5] = t; }
             else sc->sum_ls_m = t;
         }
     }
@@ -133,7 +134,7 @@ k_sum_ls(int len, const double *__restrict__ s1, const double *__restrict__ l1, 
         const double t = sum_partials(dpart, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
-            if (final_) sc->sum_ls = sc->sum_ls_m + t;
+            if (final_) { sc->sum_ls = sc->sum_ls_m + t; sc->loc[5] = t; }
             else sc->sum_ls_m = t;
         }
     }
@@ -282,12 +283,12 @@ k_resid_n(int n, int ncb, const double *__restrict__ ypart, const int64_t *__res
         const double te = sum_partials(p5, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[C_RES_N] = 0;
-            sc->rH_max = ta;
-            sc->prim_max = fmax(tb, sc->prim_max_m);
-            sc->comp_max = fmax(tc, sc->comp_max_m);
-            sc->ls_max = fmax(td, sc->ls_max_m);
-            sc->obj = te;
-            if (!finite_d(te)) sc->nonfinite = 1;
+            if (sc->sharded) {
+                sc->loc[0] = ta; sc->loc[1] = tb; sc->loc[2] = tc; sc->loc[3] = td; sc->loc[4] = te;
+                sc->loc[6] = (double)sc->nonfinite;
+            } else {
+                fin_resid(sc, ta, tb, tc, td, te);
+            }
         }
     }
 }
@@ -559,12 +560,16 @@ k_recover_n(int n, const double *__restrict__ xl, const double *__restrict__ xu,
         p2[blockIdx.x] = b;
     }
     if (last_block(&sc->counters[C_REC_N])) {
-        const double ta = fmin(min_partials(p1, gridDim.x, red), sc->minx_m);
-        const double tb = fmin(min_partials(p2, gridDim.x, red), sc->minl_m);
+        const double ta = min_partials(p1, gridDim.x, red);
+        const double tb = min_partials(p2, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[C_REC_N] = 0;
-            sc->alpha_x = fmin(1.0, tau * ta);
-            sc->alpha_l = fmin(1.0, tau * tb);
+            if (sc->sharded) {
+                sc->loc[0] = ta;
+                sc->loc[1] = tb;
+            } else {
+                fin_recover(sc, ta, tb, tau);
+            }
         }
     }
 }
@@ -631,7 +636,7 @@ k_muaff(int len, const double *__restrict__ s1, const double *__restrict__ ds1, 
         const double t = sum_partials(dpart, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
-            if (final_) sc->muaff = sc->muaff_m + t;
+            if (final_) { sc->muaff = sc->muaff_m + t; sc->loc[5] = t; }
             else sc->muaff_m = t;
         }
     }

@@ -43,6 +43,12 @@ void launch_pcg_init(const Prob &P, const Vecs &V, Scalars *sc, const double *rh
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
                           cudaGraphConditionalHandle h, int use_cond, cudaStream_t st);
 void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st);
+
+// shard.cu
+void launch_xcombine(Scalars *sc, const double *xall, int P, int stage, double p0, double p1, int64_t p2,
+                     cudaStream_t st);
 void launch_dot2(int n, const double *a, double *dpart, Scalars *sc, cudaStream_t st);  // res2 = |a|^2
 
 // ipmops.cu — per-IPM-iteration kernels (masked full-length families)

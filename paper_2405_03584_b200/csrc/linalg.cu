@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "state.h"
+#include "finalize.cuh"
 
 namespace ipm {
 
@@ -108,7 +109,8 @@ k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
-            if (MODE == 1) {
+            if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
+            if (MODE == 1 && !sc->sharded) {
                 const double pkp = tot + sc->S_b + sc->S_c;
                 sc->pKp = pkp;
                 if (!(pkp > 0.0) || !finite_d(pkp)) {
@@ -289,7 +291,8 @@ k_gemv_bulk(const double *__restrict__ H, int64_t ldh, int nrows, int ncols, con
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
-            if (MODE == 1) {
+            if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
+            if (MODE == 1 && !sc->sharded) {
                 const double pkp = tot + sc->S_b + sc->S_c;
                 sc->pKp = pkp;
                 if (!(pkp > 0.0) || !finite_d(pkp)) {
@@ -429,6 +432,7 @@ k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *_
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->res2 = tot;
+            sc->loc[4] = tot;
         }
     }
 }
@@ -616,8 +620,8 @@ __global__ void k_rank2(int nrows, int row0, int ncols, double *__restrict__ H, 
         const int i = (int)(e / ncols), j = (int)(e - (int64_t)i * ncols);
         const int gi = row0 + i;
         double h = H[(int64_t)i * ldh + j];
-        h = fma(a * u[gi], u[j], h);
-        h = fma(b * v[gi], v[j], h);
+        h = fma(a, u[gi] * u[j], h);   // u_i u_j commutes exactly: H stays bitwise symmetric
+        h = fma(b, v[gi] * v[j], h);
         H[(int64_t)i * ldh + j] = h;
         if (j == gi) diagH[i] = h;
     }

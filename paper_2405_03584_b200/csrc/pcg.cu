@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "state.h"
+#include "finalize.cuh"
 
 #include <cstdio>
 #include <cstdlib>
@@ -67,19 +68,12 @@ k_pcg_init(int n, const double *__restrict__ rhs, double *__restrict__ x, double
         const double trr = sum_partials(p2, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[C_INIT_PCG] = 0;
-            sc->rho = trz;
-            sc->rho_old = trz;
-            sc->rr = trr;
-            sc->rhs2 = trr;
-            const double t1 = rtol * rtol * trr, t2 = atol * atol;
-            sc->tol2 = t1 > t2 ? t1 : t2;
-            sc->it = 0;
-            sc->it_rs = 0;
-            sc->maxit = maxit;
-            sc->breakdown = 0;
-            sc->S_b = sc->S_c = sc->S_H = 0.0;
-            sc->done = (trr <= sc->tol2) ? 1 : 0;
-            if (!finite_d(trr) || !finite_d(trz)) { sc->done = 1; sc->breakdown = 1; }
+            if (sc->sharded) {
+                sc->loc[2] = trz;
+                sc->loc[3] = trr;
+            } else {
+                fin_pcg_init(sc, trz, trr, rtol, atol, maxit);
+            }
         }
     }
     (void)p3;
@@ -116,11 +110,12 @@ k_pcg_restart(int n, const double *__restrict__ r, double *__restrict__ z, const
         const double trr = sum_partials(p2, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[C_INIT_PCG] = 0;
-            sc->rho = trz;
-            sc->rho_old = trz;
-            sc->rr = trr;
-            sc->it_rs = 0;
-            sc->done = (trr <= sc->tol2 || sc->it >= sc->maxit) ? 1 : 0;
+            if (sc->sharded) {
+                sc->loc[2] = trz;
+                sc->loc[3] = trr;
+            } else {
+                fin_pcg_restart(sc, trz, trr);
+            }
         }
     }
 }
@@ -169,6 +164,7 @@ k_pcg_p(int n, const double *__restrict__ z, double *__restrict__ p, const doubl
         if (threadIdx.x == 0) {
             sc->counters[C_P] = 0;
             sc->S_b = t;
+            sc->loc[0] = t;
         }
     }
 }
@@ -224,18 +220,34 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
         const double trr = sum_partials(p2, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[C_UPD] = 0;
-            sc->rho_old = sc->rho;
-            sc->rho = trz;
-            sc->rr = trr;
-            sc->it += 1;
-            sc->it_rs += 1;
-            int stop = 0;
-            if (trr <= sc->tol2 || sc->it >= sc->maxit) stop = 1;
-            if (!finite_d(trr) || !finite_d(trz)) { stop = 1; sc->breakdown = 1; }
-            sc->done = stop;
-            if (use_cond) cudaGraphSetConditional(h, stop ? 0u : 1u);
+            if (sc->sharded) {
+                sc->loc[2] = trz;
+                sc->loc[3] = trr;
+            } else {
+                const int stop = fin_pcg_update(sc, trz, trr);
+                if (use_cond) cudaGraphSetConditional(h, stop ? 0u : 1u);
+            }
         }
     }
+}
+
+void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
+    k_pcg_p<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2], sc);
+}
+
+void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st) {
+    const int ug = grid_for(P.n, kBlock / G);
+    const double *t = (P.m > 0) ? V.pt : nullptr;
+#define IPM_UPD(GG)                                                                                              \
+    k_pcg_update<GG><<<ug, kBlock, 0, st>>>(P.n, ncb, V.ypart, V.sig_b, V.pp, P.ATrp, P.ATcol, P.ATval, t, x, V.pr, \
+                                            V.pz, V.Minv, V.part[5], V.part[6], sc, 0, 0)
+    switch (G) {
+        case 4: IPM_UPD(4); break;
+        case 8: IPM_UPD(8); break;
+        case 16: IPM_UPD(16); break;
+        default: IPM_UPD(32); break;
+    }
+#undef IPM_UPD
 }
 
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,

@@ -40,8 +40,17 @@ struct Scalars {
     double alpha_x, alpha_l;
     double muaff_m, muaff;       // Mehrotra affine complementarity sums
     int64_t nonfinite;           // residual/step contained Inf/NaN
+    // --- row-sharded mode ------------------------------------------------
+    // sharded = 1: last blocks write this rank's partials to loc[] and skip every derived
+    // quantity; an allgather of loc[] plus k_xcombine (rank-ordered, identical on all ranks)
+    // produces the global values.  Slot use per stage is documented in shard.cu.
+    int64_t sharded;
+    double loc[8];
     unsigned int counters[kNumCounters];
 };
+
+// Combine stages of k_xcombine (shard.cu).
+enum XStage { X_PCG_INIT = 0, X_PCG_ALPHA, X_PCG_UPDATE, X_PCG_RESTART, X_RES2, X_SUMLS, X_RESID, X_RECOVER, X_MUAFF };
 
 enum Counter {
     C_GEMV = 0, C_GEMV_PCG, C_SPMV, C_SPMV_PCG, C_P, C_UPD, C_INIT_PCG, C_TRUE_RES, C_INIT_M, C_INIT_N,
@@ -86,6 +95,8 @@ struct Vecs {
     // PCG
     double *pr, *pz, *pp, *pt, *py;                  // r, z, p (n), t (m), y (n)
     double *ypart;                                   // n x ncb GEMV tile partials
+    double *gfull;                                   // sharded: gathered full-length vector (P*chunk)
+    double *xloc_all;                                // sharded: allgathered loc[] of all ranks (8*P)
     double *part[8];                                 // reduction partials, kMaxPartials each
 };
 

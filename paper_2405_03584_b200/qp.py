@@ -49,7 +49,11 @@ class QP:
     """min 1/2 x^T H x + g^T x  s.t.  l <= A x <= u,  xl <= x <= xu   (eq:qp)."""
 
     def __init__(self, H, g, A_rowptr, A_col, A_val, l, u, xl, xu, *, ldh: Optional[int] = None,
-                 device=None, stream: Optional[torch.cuda.Stream] = None, **options):
+                 device=None, stream: Optional[torch.cuda.Stream] = None, shard: Optional[dict] = None,
+                 **options):
+        """shard (row-sharded path): dict(rank, nranks, comm_kind, handle) where
+        H holds only this rank's row block (see paper_2405_03584_b200.dist.partition) and
+        handle is a ctypes pointer to an ncclUniqueId (comm_kind 1) or an ipm_group (2)."""
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2405_03584_b200 needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -83,6 +87,17 @@ class QP:
             prob.A_rowptr, prob.A_col, prob.A_val = self.A_rowptr.data_ptr(), self.A_col.data_ptr(), self.A_val.data_ptr()
             prob.l, prob.u, prob.xl, prob.xu = self.l.data_ptr(), self.u.data_ptr(), self.xl.data_ptr(), self.xu.data_ptr()
             prob.row_begin, prob.row_end, prob.rank, prob.nranks = 0, n, 0, 1
+            self.row0, self.nloc = 0, n
+            if shard is not None:
+                from .dist import partition
+                P = int(shard["nranks"])
+                r = int(shard["rank"])
+                b, e = partition(n, P)[r]
+                prob.row_begin, prob.row_end, prob.rank, prob.nranks = b, e, r, P
+                prob.comm_kind = int(shard["comm_kind"])
+                prob.comm_handle_host = C.cast(shard["handle"], C.c_void_p)
+                self._shard_keep = shard
+                self.row0, self.nloc = b, e - b
             self._prob = prob
             self.options = make_options(**options)
             nbytes = C.c_size_t(0)
@@ -120,9 +135,9 @@ class QP:
         return L.STATUS_NAMES[st]
 
     def solution(self) -> Dict[str, torch.Tensor]:
-        out = {"x": torch.empty(self.n, dtype=torch.float64, device=self.device)}
+        out = {"x": torch.empty(self.nloc, dtype=torch.float64, device=self.device)}
         for f in _FAMILIES:
-            ln = self.m if f.endswith("A") else self.n
+            ln = self.m if f.endswith("A") else self.nloc
             out["lam_" + f] = torch.zeros(ln, dtype=torch.float64, device=self.device)
         obj = C.c_double()
         L.check(L.ipm_get_solution(self.ctx, _ptr(out["x"]), _ptr(out["lam_lA"]), _ptr(out["lam_uA"]),
@@ -182,12 +197,12 @@ class QP:
         self.stream.synchronize()
 
     def get_iterate(self):
-        x = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        x = torch.empty(self.nloc, dtype=torch.float64, device=self.device)
         s, lam = {}, {}
         sp = (C.c_void_p * 4)()
         lp = (C.c_void_p * 4)()
         for i, f in enumerate(_FAMILIES):
-            ln = self.m if f.endswith("A") else self.n
+            ln = self.m if f.endswith("A") else self.nloc
             s[f] = torch.zeros(ln, dtype=torch.float64, device=self.device)
             lam[f] = torch.zeros(ln, dtype=torch.float64, device=self.device)
             sp[i] = s[f].data_ptr()
@@ -199,19 +214,19 @@ class QP:
     # ------------------------------------------------------------------ test hooks
     def op_apply(self, sig_b, sig_c, v) -> torch.Tensor:
         sb, scv, vv = (_dev(a, torch.float64, self.device) for a in (sig_b, sig_c, v))
-        y = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        y = torch.empty(self.nloc, dtype=torch.float64, device=self.device)
         L.check(L.ipm_op_apply(self.ctx, _ptr(sb), _ptr(scv), _ptr(vv), _ptr(y)), self.ctx)
         return y
 
     def op_diag(self, sig_b, sig_c) -> torch.Tensor:
         sb, scv = (_dev(a, torch.float64, self.device) for a in (sig_b, sig_c))
-        d = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        d = torch.empty(self.nloc, dtype=torch.float64, device=self.device)
         L.check(L.ipm_op_diag(self.ctx, _ptr(sb), _ptr(scv), _ptr(d)), self.ctx)
         return d
 
     def pcg(self, sig_b, sig_c, rhs, rtol: float):
         sb, scv, r = (_dev(a, torch.float64, self.device) for a in (sig_b, sig_c, rhs))
-        x = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        x = torch.empty(self.nloc, dtype=torch.float64, device=self.device)
         it = C.c_int32()
         st = L.ipm_pcg(self.ctx, _ptr(sb), _ptr(scv), _ptr(r), _ptr(x), float(rtol), C.byref(it))
         L.check(st, self.ctx, allow=(L.IPM_OK, L.IPM_NOT_CONVERGED))

@@ -11,7 +11,7 @@ its = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 gk = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 q = config(wl, 0)
 t = problem_tensors(q, torch.device("cuda", 0))
-qp = QP(device="cuda:0", max_ipm_iter=1, pcg_max_iter=its, gemv_kernel=gk, **t)
+qp = QP(device="cuda:0", max_ipm_iter=1, pcg_max_iter=its, gemv_kernel=gk, use_graph=int(os.environ.get("USE_GRAPH", "0")), **t)
 qp.solve()
 print("gemv ms", qp.profile("gemv", 3), flush=True)
 print(qp.stats(), flush=True)

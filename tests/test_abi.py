@@ -52,13 +52,13 @@ def test_struct_sizes_match_c(lib, tmp_path):
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ipm.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu\\n",'
                    'sizeof(ipm_options), sizeof(ipm_problem), sizeof(ipm_stats), sizeof(ipm_trace_rec),'
-                   'offsetof(ipm_options, warm_shift), offsetof(ipm_problem, nccl_unique_id_host));return 0;}\n')
+                   'offsetof(ipm_options, warm_shift), offsetof(ipm_problem, comm_handle_host));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     assert vals == [C.sizeof(lib.ipm_options), C.sizeof(lib.ipm_problem), C.sizeof(lib.ipm_stats),
                     C.sizeof(lib.ipm_trace_rec), lib.ipm_options.warm_shift.offset,
-                    lib.ipm_problem.nccl_unique_id_host.offset]
+                    lib.ipm_problem.comm_handle_host.offset]
 
 
 def test_workspace_size_host_only(lib):
@@ -81,3 +81,25 @@ def test_create_without_gpu_fails_loudly(lib):
     with pytest.raises(RuntimeError):
         QP(np.eye(2), np.zeros(2), np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0), np.zeros(0),
            np.zeros(0), -np.ones(2), np.ones(2))
+
+
+def test_partition_validation_before_any_device_work(lib):
+    """ipm_create rejects a row block that is not the ceil(n/P) partition (host check, no GPU)."""
+    from paper_2405_03584_b200.dist import LocalGroup, partition
+    assert partition(10, 3) == [(0, 4), (4, 8), (8, 10)]
+    with pytest.raises(ValueError):
+        partition(5, 4)          # ceil(5/4)=2 -> ranks 0..2 cover 6 > 5 rows, rank 3 empty
+    grp = LocalGroup(3)
+    p = lib.ipm_problem()
+    p.n, p.m, p.nnz, p.ldh = 10, 0, 0, 10
+    dummy = C.c_void_p(16)
+    p.H = p.g = p.xl = p.xu = dummy
+    p.rank, p.nranks, p.comm_kind, p.comm_handle_host = 1, 3, 2, grp.handle
+    p.row_begin, p.row_end = 3, 8
+    ctx = C.c_void_p()
+    st = lib.ipm_create(C.byref(ctx), C.byref(p), None, None, 0, None)
+    assert st == lib.IPM_ERR_INVALID and b"must be [4,8)" in lib.ipm_last_error(None)
+    p.comm_kind = 0
+    st = lib.ipm_create(C.byref(ctx), C.byref(p), None, None, 0, None)
+    assert st == lib.IPM_ERR_INVALID and b"nranks > 1 needs comm_kind" in lib.ipm_last_error(None)
+    grp.close()
