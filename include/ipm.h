@@ -76,7 +76,8 @@ typedef struct {
     int32_t trace;              /* 1: record one ipm_trace_rec per IPM iteration */
     int32_t use_graph;          /* 1: PCG loop as a CUDA graph with a device-side WHILE node */
     double warm_shift;          /* 1e-3   theta of the warm-start rule (R15) */
-    int32_t gemv_kernel;        /* 0 auto, 1 LDG.128 register tiles, 2 TMA-bulk mbarrier pipeline */
+    int32_t gemv_kernel;        /* 0 auto (3 when H == H^T bitwise and unsharded, else 2), 1 LDG.128 register
+                                   tiles, 2 TMA-bulk mbarrier pipeline, 3 symmetric upper-triangle TMA-bulk */
 } ipm_options;
 
 /* Problem description for ipm_create.  Large arrays are BORROWED (the caller keeps them

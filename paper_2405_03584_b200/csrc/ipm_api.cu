@@ -89,7 +89,7 @@ Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks
     o.sc = L.take(sizeof(Scalars));
     for (int i = 0; i < kNVec; ++i) o.nvec[i] = L.take(sizeof(double) * (std::max<int64_t>(chunk, 1) + 2));
     for (int i = 0; i < kMVec; ++i) o.mvec[i] = L.take(sizeof(double) * std::max<int64_t>(m, 1));
-    o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) * gemv_ncb((int)ncols));
+    o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) * std::max(gemv_ncb((int)ncols), sym_ncb((int)ncols)));
     o.part = L.take(sizeof(double) * kMaxPartials * 8);
     o.ATrp = L.take(sizeof(int64_t) * (nloc + 1));
     o.ATcol = L.take(sizeof(int) * std::max<int64_t>(nnz_loc, 1));
@@ -802,13 +802,33 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         CK(cudaMemcpyAsync(&nbad, bad, sizeof nbad, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
         if (nbad) { s = fail(ctx, IPM_ERR_INVALID, "H has %llu non-finite entries", nbad); return s; }
-        ctx->ncb = gemv_ncb((int)p->n);
         ctx->gemv_grid = gemv_max_grid();
         const int gk = ctx->opt.gemv_kernel;
-        P.gemv_bulk = (gk == 2 || gk == 0) && gemv_bulk_ok(P) ? 1 : 0;
-        if (gk == 2 && !P.gemv_bulk) { s = fail(ctx, IPM_ERR_INVALID, "gemv_kernel=2 needs even ldh and 16-byte aligned H"); return s; }
+        const bool bulk_ok = gemv_bulk_ok(P);
+        bool sym = false;
+        if ((gk == 0 || gk == 3) && !ctx->sharded && bulk_ok) {
+            // the symmetric GEMV reads only H's upper block triangle: require H == H^T bitwise
+            unsigned long long nasym = 0;
+            CK(cudaMemsetAsync(bad, 0, sizeof nasym, ctx->st));
+            launch_count_asym(P, bad, ctx->st);
+            CKL();
+            CK(cudaMemcpyAsync(&nasym, bad, sizeof nasym, cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            sym = (nasym == 0);
+            ctx->launches += 1;
+        }
+        if (gk == 3 && !sym)
+            return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=3 needs an unsharded, exactly symmetric H with even ldh");
+        if (gk == 2 && !bulk_ok) return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=2 needs even ldh and 16-byte aligned H");
+        P.gemv_sym = sym ? 1 : 0;
+        P.gemv_bulk = (!sym && (gk == 0 || gk == 2) && bulk_ok) ? 1 : 0;
         P.gemv_bulk_grid = gemv_bulk_grid();
+        ctx->ncb = sym ? sym_ncb((int)p->n) : gemv_ncb((int)p->n);
+        P.ncb = ctx->ncb;
         ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
+        DBG("create: n=%lld m=%lld nnz=%lld gemv=%s ncb=%d G=%d sharded=%d\n", (long long)p->n, (long long)p->m,
+            (long long)p->nnz, sym ? "symmetric-bulk" : (P.gemv_bulk ? "bulk" : "ldg"), ctx->ncb, ctx->G,
+            (int)ctx->sharded);
     
     return IPM_OK;
 }

@@ -303,7 +303,7 @@ k_resid_n(int n, int ncb, const double *__restrict__ ypart, const int64_t *__res
 
 // Requires: V.ypart holds the GEMV tiles of H x and V.Ax = A x (launched by the caller).
 void launch_residuals(const Prob &P, const Vecs &V, int G, Scalars *sc, double mu, cudaStream_t st) {
-    const int ncb = gemv_ncb(P.ncols);
+    const int ncb = P.ncb;
     cudaMemsetAsync(&sc->prim_max_m, 0, 3 * sizeof(double) * 2, st);   // *_max_m and neighbours
     if (P.m > 0)
         k_resid_m<<<grid_for(P.m, kBlock), kBlock, 0, st>>>(P.m, P.l, P.u, V.Ax, V.s_lA, V.s_uA, V.lam_lA, V.lam_uA,

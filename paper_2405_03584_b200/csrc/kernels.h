@@ -15,12 +15,17 @@ constexpr int kGemvRB = 16;         // rows per GEMV tile
 constexpr int kGemvCW = 1024;       // columns per GEMV tile (8 KB of the vector in smem)
 
 inline int gemv_ncb(int ncols) { return (ncols + kGemvCW - 1) / kGemvCW; }
+constexpr int kSymB = 256;          // symmetric GEMV: square B x B blocks of H
+inline int sym_ncb(int n) { return (n + kSymB - 1) / kSymB; }
 
 // linalg.cu
 void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb,
                  double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
 int gemv_max_grid();
 bool gemv_bulk_ok(const Prob &P);
+void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
+                      int grid, int mode, int cid, cudaStream_t st);
+void launch_count_asym(const Prob &P, unsigned long long *bad, cudaStream_t st);
 int gemv_bulk_grid();
 void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb, double *dpart,
                       Scalars *sc, int grid, int mode, int cid, cudaStream_t st);

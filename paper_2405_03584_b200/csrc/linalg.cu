@@ -129,6 +129,10 @@ void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypa
                  double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st) {
     const bool vec = ((P.ldh & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.H) & 15) == 0);
     if (P.n == 0) return;
+    if (P.gemv_sym) {
+        launch_symv_bulk(P, v, vdot, ypart, dpart, sc, P.gemv_bulk_grid, mode, cid, st);
+        return;
+    }
     if (P.gemv_bulk) {
         launch_gemv_bulk(P, v, vdot, ypart, ncb, dpart, sc, P.gemv_bulk_grid, mode, cid, st);
         return;
@@ -331,6 +335,195 @@ void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double
         k_gemv_bulk<1><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
     else
         k_gemv_bulk<0><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+}
+
+// ------------------------------------------------------- symmetric GEMV (upper block triangle)
+// H is symmetric (SPD, checked bitwise at create): y = H p needs only the blocks H_IJ with
+// I <= J of the resident full matrix.  Each such kSymB x kSymB tile is streamed ONCE (TMA
+// bulk copies, kSymSR rows per pipeline stage) and applied twice:
+//   row part   (H_IJ   p_J)_i  -> ypart[i][J]            (every tile, incl. the diagonal)
+//   column part(H_IJ^T p_I)_j  -> ypart[j][I]            (off-diagonal tiles only)
+// so every slot of ypart[row][0..nb) is written exactly once (block J >= I(row) by a row
+// part, J < I(row) by a column part) and the consumers sum it in fixed order: deterministic,
+// 4 n^2 + O(n kSymB) bytes per apply instead of 8 n^2.  Consumer thread c owns column c of
+// the tile and accumulates its column part over the strips in a register; warp w reduces
+// rows w and w+8 of each strip.  Tiles (row-major over the upper triangle) are split among
+// the persistent CTAs as contiguous ranges.
+constexpr int kSymSR = 16;
+constexpr int kSymStages = 6;
+constexpr int kSymStageDoubles = kSymSR * kSymB + kSymB + kSymSR;
+constexpr size_t kSymSmem = (size_t)kSymStages * kSymStageDoubles * 8 + 2 * kSymStages * 8;
+static_assert(kBulkConsumers * 32 == kSymB, "one consumer thread per tile column");
+
+__device__ __forceinline__ void sym_locate(int64_t t, int nb, int &I, int &J) {
+    int i = 0;
+    int64_t c = 0;
+    while (c + (nb - i) <= t) {
+        c += nb - i;
+        ++i;
+    }
+    I = i;
+    J = i + (int)(t - c);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+k_symv_bulk(const double *__restrict__ H, int64_t ldh, int n, const double *__restrict__ p,
+            const double *__restrict__ pdot, double *__restrict__ ypart, int nb, double *__restrict__ dpart,
+            Scalars *sc, int cid) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[kBulkThreads / 32];
+    if (MODE == 1 && sc->done) return;
+    double *stages = reinterpret_cast<double *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kSymStages * kSymStageDoubles * 8);
+    uint64_t *empty = full + kSymStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSymStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kBulkConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t ntiles = (int64_t)nb * (nb + 1) / 2;
+    const int64_t t0 = ntiles * blockIdx.x / gridDim.x;
+    const int64_t t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+    double dacc = 0.0;
+    int I = 0, J = 0;
+    if (t0 < t1) sym_locate(t0, nb, I, J);
+    if (warp == kBulkConsumers) {
+        if (lane == 0) {
+            uint64_t pol_h, pol_p;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_h));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_p));
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = t0; t < t1; ++t) {
+                const int rowsI = min(kSymB, n - I * kSymB);
+                const int colsJ = min(kSymB, n - J * kSymB);
+                const int cwb = (colsJ + 1) & ~1;
+                for (int s0 = 0; s0 < rowsI; s0 += kSymSR) {
+                    const int rows = min(kSymSR, rowsI - s0);
+                    const int rb = (rows + 1) & ~1;
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    double *sH = stages + (size_t)stage * kSymStageDoubles;
+                    double *sPJ = sH + kSymSR * kSymB;
+                    double *sPI = sPJ + kSymB;
+                    mbar_expect_tx(&full[stage], (uint32_t)((rows * cwb + cwb + rb) * 8));
+                    const double *src = H + (int64_t)(I * kSymB + s0) * ldh + (int64_t)J * kSymB;
+                    for (int r = 0; r < rows; ++r)
+                        bulk_g2s(sH + r * kSymB, src + (int64_t)r * ldh, (uint32_t)(cwb * 8), &full[stage], pol_h);
+                    bulk_g2s(sPJ, p + (int64_t)J * kSymB, (uint32_t)(cwb * 8), &full[stage], pol_p);
+                    bulk_g2s(sPI, p + (int64_t)I * kSymB + s0, (uint32_t)(rb * 8), &full[stage], pol_p);
+                    if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
+                }
+                if (++J == nb) { ++I; J = I; }
+            }
+        }
+        __syncwarp();
+    } else {
+        const int c = threadIdx.x;            // tile column owned by this thread
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            const int rowsI = min(kSymB, n - I * kSymB);
+            const int colsJ = min(kSymB, n - J * kSymB);
+            const bool diag = (I == J);
+            double colacc = 0.0;
+            for (int s0 = 0; s0 < rowsI; s0 += kSymSR) {
+                const int rows = min(kSymSR, rowsI - s0);
+                mbar_wait(&full[stage], phase);
+                const double *sH = stages + (size_t)stage * kSymStageDoubles;
+                const double *sPJ = sH + kSymSR * kSymB;
+                const double *sPI = sPJ + kSymB;
+                // row part: rows warp and warp + 8 of the strip
+                for (int rr = warp; rr < rows; rr += kBulkConsumers) {
+                    const double2 *hv = reinterpret_cast<const double2 *>(sH + rr * kSymB);
+                    const double2 *pv = reinterpret_cast<const double2 *>(sPJ);
+                    double a = 0.0, b = 0.0;
+#pragma unroll 4
+                    for (int k = lane; k < (colsJ >> 1); k += 32) {
+                        const double2 h = hv[k], q = pv[k];
+                        a = fma(h.x, q.x, a);
+                        b = fma(h.y, q.y, b);
+                    }
+                    if ((colsJ & 1) && lane == 0) a = fma(sH[rr * kSymB + colsJ - 1], sPJ[colsJ - 1], a);
+                    const double s = warp_sum(a + b);
+                    if (lane == 0) {
+                        const int row = I * kSymB + s0 + rr;
+                        ypart[(int64_t)row * nb + J] = s;
+                        if (pdot) dacc = fma(pdot[row], s, dacc);
+                    }
+                }
+                // column part (H_IJ^T p_I) for this thread's column
+                if (!diag && c < colsJ) {
+#pragma unroll 4
+                    for (int r = 0; r < rows; ++r) colacc = fma(sH[r * kSymB + c], sPI[r], colacc);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+                if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
+            }
+            if (!diag && c < colsJ) {
+                const int j = J * kSymB + c;
+                ypart[(int64_t)j * nb + I] = colacc;
+                if (pdot) dacc = fma(pdot[j], colacc, dacc);
+            }
+            if (++J == nb) { ++I; J = I; }
+        }
+    }
+    if (pdot == nullptr) return;
+    const double bs = block_sum(dacc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
+    if (last_block(&sc->counters[cid])) {
+        const double tot = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[cid] = 0;
+            sc->S_H = tot;
+            if (sc->sharded) sc->loc[1] = tot;
+            if (MODE == 1 && !sc->sharded) fin_pcg_alpha(sc, tot + sc->S_b + sc->S_c);
+        }
+    }
+}
+
+void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
+                      int grid, int mode, int cid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_symv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
+        cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
+        attr = true;
+    }
+    const int nb = sym_ncb(P.n);
+    if (mode == 1)
+        k_symv_bulk<1><<<grid, kBulkThreads, kSymSmem, st>>>(P.H, P.ldh, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+    else
+        k_symv_bulk<0><<<grid, kBulkThreads, kSymSmem, st>>>(P.H, P.ldh, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+}
+
+// Exact-symmetry check at create (the symmetric GEMV is only used when H == H^T bitwise).
+__global__ void k_count_asym(int n, const double *__restrict__ H, int64_t ldh, unsigned long long *bad) {
+    __shared__ double a[32][33], b[32][33];
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    if (bj < bi) return;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int i1 = bi * 32 + r, j1 = bj * 32 + tx;
+        a[r][tx] = (i1 < n && j1 < n) ? H[(int64_t)i1 * ldh + j1] : 0.0;
+        const int i2 = bj * 32 + r, j2 = bi * 32 + tx;
+        b[r][tx] = (i2 < n && j2 < n) ? H[(int64_t)i2 * ldh + j2] : 0.0;
+    }
+    __syncthreads();
+    unsigned long long cnt = 0;
+    for (int r = ty; r < 32; r += blockDim.y)
+        if (a[r][tx] != b[tx][r]) ++cnt;
+    if (cnt) atomicAdd(bad, cnt);
+}
+
+void launch_count_asym(const Prob &P, unsigned long long *bad, cudaStream_t st) {
+    const int nb32 = (P.n + 31) / 32;
+    k_count_asym<<<dim3(nb32, nb32), dim3(32, 8), 0, st>>>(P.n, P.H, P.ldh, bad);
 }
 
 // ------------------------------------------------------------------------------ SpMV (A v)

@@ -75,6 +75,8 @@ struct Prob {
     double *diagH;
     int gemv_bulk;         // 1: use the TMA-bulk GEMV (k_gemv_bulk) with grid gemv_bulk_grid
     int gemv_bulk_grid;
+    int gemv_sym;          // 1: symmetric upper-triangle TMA-bulk GEMV (k_symv_bulk)
+    int ncb;               // column blocks of the ypart[row][cb] layout of the chosen GEMV
 };
 
 // Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).

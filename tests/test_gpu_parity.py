@@ -77,7 +77,36 @@ def test_gemv_kernels_agree_bitwise(n):
     assert np.linalg.norm(yb.cpu().numpy() - yref) <= 1e-12 * np.linalg.norm(yref)
 
 
-@pytest.mark.parametrize("gk", [1, 2])
+@pytest.mark.parametrize("n,m", [(1, 1), (255, 30), (256, 0), (1000, 200), (2049, 500), (5003, 300)])
+def test_symmetric_gemv_matches_oracle(n, m):
+    """gemv_kernel=3 reads only the upper block triangle of the (exactly symmetric) H."""
+    q = planted_qp(n, m, density=min(1.0, 0.02 + 2.0 / n), rank=min(48, n), seed=n + 3 * m,
+                   rows="mixed" if m else "vmat", var="mixed")
+    qp = _qp(q, gemv_kernel=3)
+    sb, sc, v = _rand_sigmas(q, 4)
+    y = qp.op_apply(sb, sc, v).cpu().numpy()
+    yref = okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v, dtype=np.longdouble).astype(np.float64)
+    assert np.linalg.norm(y - yref) <= 1e-12 * np.linalg.norm(yref)
+    # and it is the auto choice for a symmetric H
+    assert _qp(q).profile("gemv", 1) > 0
+
+
+def test_symmetric_gemv_rejected_for_asymmetric_H():
+    from paper_2405_03584_b200 import QP, _lib
+    q = planted_qp(300, 20, density=0.05, rank=16, seed=1)
+    t = problem_tensors(q, DEV)
+    t["H"][3, 7] += 1e-3          # H != H^T
+    with pytest.raises(_lib.IpmError, match="symmetric"):
+        QP(device=DEV, gemv_kernel=3, **t)
+    qp = QP(device=DEV, **t)      # auto falls back to the full GEMV and stays exact
+    sb, sc, v = _rand_sigmas(q, 1)
+    H = t["H"][:, :q.n].cpu().numpy()
+    yref = okkt.condensed_apply(H, q.A_dense(), sb, sc, v, dtype=np.longdouble).astype(np.float64)
+    y = qp.op_apply(sb, sc, v).cpu().numpy()
+    assert np.linalg.norm(y - yref) <= 1e-12 * np.linalg.norm(yref)
+
+
+@pytest.mark.parametrize("gk", [1, 2, 3])
 def test_ipm_both_gemv_kernels(gk):
     q = planted_qp(1500, 300, density=0.02, rank=32, seed=11, rows="vmat", var="box")
     _check_against_oracle(q, dict(gemv_kernel=gk))
