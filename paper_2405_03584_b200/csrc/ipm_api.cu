@@ -141,6 +141,7 @@ struct ipm_ctx {
     std::string err;
     int64_t launches = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    alignas(64) unsigned char tmap_sym[128] = {};   // CUtensorMap for the symmetric GEMV
     // row-sharded mode
     ipm::Comm *comm = nullptr;
     bool sharded = false;
@@ -816,6 +817,10 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             CK(cudaStreamSynchronize(ctx->st));
             sym = (nasym == 0);
             ctx->launches += 1;
+            if (sym) {
+                sym = make_sym_tensor_map(P, ctx->tmap_sym);
+                P.tmap_sym = ctx->tmap_sym;
+            }
         }
         if (gk == 3 && !sym)
             return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=3 needs an unsharded, exactly symmetric H with even ldh");
@@ -1025,7 +1030,8 @@ IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, doub
     CK(cudaMemsetAsync(&ctx->sc->done, 0, sizeof(int64_t), ctx->st));
     CK(cudaMemsetAsync(&ctx->sc->it_rs, 0, sizeof(int64_t), ctx->st));
     auto one = [&]() {
-        if (what == 0) launch_gemv(P, V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, ctx->st);
+        // what 0: the PCG GEMV's full work (tiles + fused p^T H p) without its done/alpha epilogue
+        if (what == 0) launch_gemv(P, V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV_PCG, ctx->st);
         else if (what == 1) launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
         else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st);
     };

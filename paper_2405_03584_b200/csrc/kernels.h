@@ -26,6 +26,7 @@ bool gemv_bulk_ok(const Prob &P);
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
                       int grid, int mode, int cid, cudaStream_t st);
 void launch_count_asym(const Prob &P, unsigned long long *bad, cudaStream_t st);
+bool make_sym_tensor_map(const Prob &P, void *out128);   // CUtensorMap (128 B, 64-B aligned)
 int gemv_bulk_grid();
 void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb, double *dpart,
                       Scalars *sc, int grid, int mode, int cid, cudaStream_t st);

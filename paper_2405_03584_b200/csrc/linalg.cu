@@ -19,6 +19,9 @@
 //   * group SpMV^T  : A^T t through the stored transpose ("pre-compute and store their
 //                     transposes ... transpose-free SpMV"), a G-lane group per row of A^T,
 //                     fused into the consumers (PCG update, residuals, RHS, colsq).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "state.h"
@@ -366,9 +369,40 @@ __device__ __forceinline__ void sym_locate(int64_t t, int nb, int &I, int &J) {
     J = i + (int)(t - c);
 }
 
+__device__ __forceinline__ void tma_2d_g2s(void *dst, const CUtensorMap *tmap, int x, int y, uint64_t *bar,
+                                           uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// Tensor map over the row-major n x n (local rows x n) fp64 matrix H: boxes of kSymSR rows x
+// kSymB columns, out-of-range elements zero-filled by the TMA unit.
+bool make_sym_tensor_map(const Prob &P, void *out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)P.ncols, (cuuint64_t)P.n};
+    const cuuint64_t strides[1] = {(cuuint64_t)P.ldh * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)kSymB, (cuuint32_t)kSymSR};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap *>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, P.H, dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kBulkThreads, 1)
-k_symv_bulk(const double *__restrict__ H, int64_t ldh, int n, const double *__restrict__ p,
+k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__restrict__ p,
             const double *__restrict__ pdot, double *__restrict__ ypart, int nb, double *__restrict__ dpart,
             Scalars *sc, int cid) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -410,10 +444,9 @@ k_symv_bulk(const double *__restrict__ H, int64_t ldh, int n, const double *__re
                     double *sH = stages + (size_t)stage * kSymStageDoubles;
                     double *sPJ = sH + kSymSR * kSymB;
                     double *sPI = sPJ + kSymB;
-                    mbar_expect_tx(&full[stage], (uint32_t)((rows * cwb + cwb + rb) * 8));
-                    const double *src = H + (int64_t)(I * kSymB + s0) * ldh + (int64_t)J * kSymB;
-                    for (int r = 0; r < rows; ++r)
-                        bulk_g2s(sH + r * kSymB, src + (int64_t)r * ldh, (uint32_t)(cwb * 8), &full[stage], pol_h);
+                    // one 2-D TMA per strip: kSymSR x kSymB box (OOB rows/cols zero-filled, full box bytes)
+                    mbar_expect_tx(&full[stage], (uint32_t)((kSymSR * kSymB + cwb + rb) * 8));
+                    tma_2d_g2s(sH, &tmap, J * kSymB, I * kSymB + s0, &full[stage], pol_h);
                     bulk_g2s(sPJ, p + (int64_t)J * kSymB, (uint32_t)(cwb * 8), &full[stage], pol_p);
                     bulk_g2s(sPI, p + (int64_t)I * kSymB + s0, (uint32_t)(rb * 8), &full[stage], pol_p);
                     if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
@@ -496,10 +529,11 @@ void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double
         attr = true;
     }
     const int nb = sym_ncb(P.n);
+    const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(P.tmap_sym);
     if (mode == 1)
-        k_symv_bulk<1><<<grid, kBulkThreads, kSymSmem, st>>>(P.H, P.ldh, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+        k_symv_bulk<1><<<grid, kBulkThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
     else
-        k_symv_bulk<0><<<grid, kBulkThreads, kSymSmem, st>>>(P.H, P.ldh, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+        k_symv_bulk<0><<<grid, kBulkThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
 }
 
 // Exact-symmetry check at create (the symmetric GEMV is only used when H == H^T bitwise).

@@ -77,6 +77,7 @@ struct Prob {
     int gemv_bulk_grid;
     int gemv_sym;          // 1: symmetric upper-triangle TMA-bulk GEMV (k_symv_bulk)
     int ncb;               // column blocks of the ypart[row][cb] layout of the chosen GEMV
+    const void *tmap_sym;  // host copy of the CUtensorMap over H (16 x 256 fp64 boxes)
 };
 
 // Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).
