@@ -456,6 +456,10 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
         }
         __syncwarp();
     } else {
+        // Latency matters more than bandwidth here (2 KB rows): every operand comes from the
+        // stage in shared memory (including the p entries of the fused p^T H p), the two rows
+        // of a warp share one interleaved shuffle tree, and the column sums use two chains.
+        static_assert(kSymSR == 2 * kBulkConsumers, "two strip rows per consumer warp");
         const int c = threadIdx.x;            // tile column owned by this thread
         int stage = 0;
         uint32_t phase = 0;
@@ -463,45 +467,67 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
             const int rowsI = min(kSymB, n - I * kSymB);
             const int colsJ = min(kSymB, n - J * kSymB);
             const bool diag = (I == J);
-            double colacc = 0.0;
+            double ce = 0.0, co = 0.0, pj_c = 0.0;
             for (int s0 = 0; s0 < rowsI; s0 += kSymSR) {
                 const int rows = min(kSymSR, rowsI - s0);
                 mbar_wait(&full[stage], phase);
                 const double *sH = stages + (size_t)stage * kSymStageDoubles;
                 const double *sPJ = sH + kSymSR * kSymB;
                 const double *sPI = sPJ + kSymB;
-                // row part: rows warp and warp + 8 of the strip
-                for (int rr = warp; rr < rows; rr += kBulkConsumers) {
-                    const double2 *hv = reinterpret_cast<const double2 *>(sH + rr * kSymB);
-                    const double2 *pv = reinterpret_cast<const double2 *>(sPJ);
-                    double a = 0.0, b = 0.0;
-#pragma unroll 4
-                    for (int k = lane; k < (colsJ >> 1); k += 32) {
-                        const double2 h = hv[k], q = pv[k];
-                        a = fma(h.x, q.x, a);
-                        b = fma(h.y, q.y, b);
-                    }
-                    if ((colsJ & 1) && lane == 0) a = fma(sH[rr * kSymB + colsJ - 1], sPJ[colsJ - 1], a);
-                    const double s = warp_sum(a + b);
-                    if (lane == 0) {
-                        const int row = I * kSymB + s0 + rr;
-                        ypart[(int64_t)row * nb + J] = s;
-                        if (pdot) dacc = fma(pdot[row], s, dacc);
+                if (s0 == 0 && c < colsJ) pj_c = sPJ[c];
+                // row part: rows r0 = warp and r1 = warp + 8 of the strip (OOB rows are zero)
+                const int r0 = warp, r1 = warp + kBulkConsumers;
+                const double2 *h0 = reinterpret_cast<const double2 *>(sH + r0 * kSymB);
+                const double2 *h1 = reinterpret_cast<const double2 *>(sH + r1 * kSymB);
+                const double2 *pv = reinterpret_cast<const double2 *>(sPJ);
+                double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int k = lane; k < kSymB / 2; k += 32) {
+                    if (k < (colsJ >> 1)) {
+                        const double2 q = pv[k], x0 = h0[k], x1 = h1[k];
+                        a0 = fma(x0.x, q.x, a0);
+                        b0 = fma(x0.y, q.y, b0);
+                        a1 = fma(x1.x, q.x, a1);
+                        b1 = fma(x1.y, q.y, b1);
                     }
                 }
-                // column part (H_IJ^T p_I) for this thread's column
+                if ((colsJ & 1) && lane == 0) {
+                    a0 = fma(sH[r0 * kSymB + colsJ - 1], sPJ[colsJ - 1], a0);
+                    a1 = fma(sH[r1 * kSymB + colsJ - 1], sPJ[colsJ - 1], a1);
+                }
+                double s0v = a0 + b0, s1v = a1 + b1;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    s0v += __shfl_xor_sync(0xffffffffu, s0v, o);
+                    s1v += __shfl_xor_sync(0xffffffffu, s1v, o);
+                }
+                if (lane == 0) {
+                    const int row = I * kSymB + s0;
+                    if (r0 < rows) {
+                        ypart[(int64_t)(row + r0) * nb + J] = s0v;
+                        if (pdot) dacc = fma(sPI[r0], s0v, dacc);
+                    }
+                    if (r1 < rows) {
+                        ypart[(int64_t)(row + r1) * nb + J] = s1v;
+                        if (pdot) dacc = fma(sPI[r1], s1v, dacc);
+                    }
+                }
+                // column part (H_IJ^T p_I) for this thread's column: even / odd rows
                 if (!diag && c < colsJ) {
-#pragma unroll 4
-                    for (int r = 0; r < rows; ++r) colacc = fma(sH[r * kSymB + c], sPI[r], colacc);
+#pragma unroll
+                    for (int r = 0; r < kSymSR; r += 2) {
+                        if (r < rows) ce = fma(sH[r * kSymB + c], sPI[r], ce);
+                        if (r + 1 < rows) co = fma(sH[(r + 1) * kSymB + c], sPI[r + 1], co);
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
                 if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
             }
             if (!diag && c < colsJ) {
-                const int j = J * kSymB + c;
-                ypart[(int64_t)j * nb + I] = colacc;
-                if (pdot) dacc = fma(pdot[j], colacc, dacc);
+                const double colacc = ce + co;
+                ypart[(int64_t)(J * kSymB + c) * nb + I] = colacc;
+                if (pdot) dacc = fma(pj_c, colacc, dacc);
             }
             if (++J == nb) { ++I; J = I; }
         }
