@@ -352,8 +352,9 @@ void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double
 // the tile and accumulates its column part over the strips in a register; warp w reduces
 // rows w and w+8 of each strip.  Tiles (row-major over the upper triangle) are split among
 // the persistent CTAs as contiguous ranges.
-constexpr int kSymSR = 16;
-constexpr int kSymStages = 6;
+constexpr int kSymSR = 32;
+constexpr int kSymStages = 3;
+constexpr int kSymRW = kSymSR / kBulkConsumers;   // strip rows reduced by each consumer warp
 constexpr int kSymStageDoubles = kSymSR * kSymB + kSymB + kSymSR;
 constexpr size_t kSymSmem = (size_t)kSymStages * kSymStageDoubles * 8 + 2 * kSymStages * 8;
 static_assert(kBulkConsumers * 32 == kSymB, "one consumer thread per tile column");
@@ -459,7 +460,6 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
         // Latency matters more than bandwidth here (2 KB rows): every operand comes from the
         // stage in shared memory (including the p entries of the fused p^T H p), the two rows
         // of a warp share one interleaved shuffle tree, and the column sums use two chains.
-        static_assert(kSymSR == 2 * kBulkConsumers, "two strip rows per consumer warp");
         const int c = threadIdx.x;            // tile column owned by this thread
         int stage = 0;
         uint32_t phase = 0;
@@ -467,7 +467,8 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
             const int rowsI = min(kSymB, n - I * kSymB);
             const int colsJ = min(kSymB, n - J * kSymB);
             const bool diag = (I == J);
-            double ce = 0.0, co = 0.0, pj_c = 0.0;
+            double cacc[4] = {0.0, 0.0, 0.0, 0.0};
+            double pj_c = 0.0;
             for (int s0 = 0; s0 < rowsI; s0 += kSymSR) {
                 const int rows = min(kSymSR, rowsI - s0);
                 mbar_wait(&full[stage], phase);
@@ -475,57 +476,59 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                 const double *sPJ = sH + kSymSR * kSymB;
                 const double *sPI = sPJ + kSymB;
                 if (s0 == 0 && c < colsJ) pj_c = sPJ[c];
-                // row part: rows r0 = warp and r1 = warp + 8 of the strip (OOB rows are zero)
-                const int r0 = warp, r1 = warp + kBulkConsumers;
-                const double2 *h0 = reinterpret_cast<const double2 *>(sH + r0 * kSymB);
-                const double2 *h1 = reinterpret_cast<const double2 *>(sH + r1 * kSymB);
+                // row part: rows warp + 8 k (k < kSymRW) of the strip (OOB rows are zero-filled)
                 const double2 *pv = reinterpret_cast<const double2 *>(sPJ);
-                double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+                double a[kSymRW], b[kSymRW];
+#pragma unroll
+                for (int q = 0; q < kSymRW; ++q) a[q] = b[q] = 0.0;
 #pragma unroll
                 for (int k = lane; k < kSymB / 2; k += 32) {
                     if (k < (colsJ >> 1)) {
-                        const double2 q = pv[k], x0 = h0[k], x1 = h1[k];
-                        a0 = fma(x0.x, q.x, a0);
-                        b0 = fma(x0.y, q.y, b0);
-                        a1 = fma(x1.x, q.x, a1);
-                        b1 = fma(x1.y, q.y, b1);
+                        const double2 pk = pv[k];
+#pragma unroll
+                        for (int q = 0; q < kSymRW; ++q) {
+                            const double2 x = reinterpret_cast<const double2 *>(sH + (warp + q * kBulkConsumers) * kSymB)[k];
+                            a[q] = fma(x.x, pk.x, a[q]);
+                            b[q] = fma(x.y, pk.y, b[q]);
+                        }
                     }
                 }
                 if ((colsJ & 1) && lane == 0) {
-                    a0 = fma(sH[r0 * kSymB + colsJ - 1], sPJ[colsJ - 1], a0);
-                    a1 = fma(sH[r1 * kSymB + colsJ - 1], sPJ[colsJ - 1], a1);
+#pragma unroll
+                    for (int q = 0; q < kSymRW; ++q)
+                        a[q] = fma(sH[(warp + q * kBulkConsumers) * kSymB + colsJ - 1], sPJ[colsJ - 1], a[q]);
                 }
-                double s0v = a0 + b0, s1v = a1 + b1;
+                double s[kSymRW];
+#pragma unroll
+                for (int q = 0; q < kSymRW; ++q) s[q] = a[q] + b[q];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
-                    s0v += __shfl_xor_sync(0xffffffffu, s0v, o);
-                    s1v += __shfl_xor_sync(0xffffffffu, s1v, o);
+#pragma unroll
+                    for (int q = 0; q < kSymRW; ++q) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
                 }
                 if (lane == 0) {
                     const int row = I * kSymB + s0;
-                    if (r0 < rows) {
-                        ypart[(int64_t)(row + r0) * nb + J] = s0v;
-                        if (pdot) dacc = fma(sPI[r0], s0v, dacc);
-                    }
-                    if (r1 < rows) {
-                        ypart[(int64_t)(row + r1) * nb + J] = s1v;
-                        if (pdot) dacc = fma(sPI[r1], s1v, dacc);
+#pragma unroll
+                    for (int q = 0; q < kSymRW; ++q) {
+                        const int r = warp + q * kBulkConsumers;
+                        if (r < rows) {
+                            ypart[(int64_t)(row + r) * nb + J] = s[q];
+                            if (pdot) dacc = fma(sPI[r], s[q], dacc);
+                        }
                     }
                 }
-                // column part (H_IJ^T p_I) for this thread's column: even / odd rows
+                // column part (H_IJ^T p_I) for this thread's column: four interleaved chains
                 if (!diag && c < colsJ) {
 #pragma unroll
-                    for (int r = 0; r < kSymSR; r += 2) {
-                        if (r < rows) ce = fma(sH[r * kSymB + c], sPI[r], ce);
-                        if (r + 1 < rows) co = fma(sH[(r + 1) * kSymB + c], sPI[r + 1], co);
-                    }
+                    for (int r = 0; r < kSymSR; ++r)
+                        if (r < rows) cacc[r & 3] = fma(sH[r * kSymB + c], sPI[r], cacc[r & 3]);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
                 if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
             }
             if (!diag && c < colsJ) {
-                const double colacc = ce + co;
+                const double colacc = (cacc[0] + cacc[1]) + (cacc[2] + cacc[3]);
                 ypart[(int64_t)(J * kSymB + c) * nb + I] = colacc;
                 if (pdot) dacc = fma(pj_c, colacc, dacc);
             }
