@@ -216,15 +216,29 @@ def run_ours(args):
     statuses = sorted(set(s["status"] for s in stats))
 
     # --- roofline of the dominant kernel (the PCG GEMV), CUDA events on our stream -------
+    info = qp.info()
     gemv_ms = qp.profile("gemv", reps=10 if n >= 10000 else 50)
     pcg_iter_ms = qp.profile("pcg_iter", reps=10 if n >= 10000 else 50)
-    gemv_bytes = 8.0 * n * n + 8.0 * n + 8.0 * n * ((n + 1023) // 1024)   # H + p + tile partials
+    ncb = info["ncb"]
+    if info["gemv_kernel"] == 3:
+        # symmetric GEMV streams the upper block triangle of H (kSymB = 256 blocks, diagonal
+        # blocks whole): algorithmic bytes = 8 * sum over tiles I <= J of rows_I * cols_J
+        B = 256
+        sizes = [min(B, n - i * B) for i in range(ncb)]
+        tri = sum(sizes[i] * sizes[j] for i in range(ncb) for j in range(i, ncb))
+        gemv_bytes = 8.0 * tri + 8.0 * n + 8.0 * n * ncb
+        kname = "k_symv_bulk<1> (symmetric upper-triangle GEMV, 2-D TMA, p^T H p fused)"
+    else:
+        gemv_bytes = 8.0 * n * n + 8.0 * n + 8.0 * n * ncb   # H + p + tile partials
+        kname = ("k_gemv_bulk<1> (TMA-bulk GEMV, p^T H p fused)" if info["gemv_kernel"] == 2
+                 else "k_gemv_tiles<1,1> (LDG.128 GEMV, p^T H p fused)")
     peak, peak_src = _peaks()
     achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
+    effective = 8.0 * n * n / (gemv_ms * 1e-3) / 1e9          # dense-H-equivalent rate
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemv_traffic.json")
     if os.path.exists(tp):
-        tj = json.load(open(tp)).get(args.workload)
+        tj = json.load(open(tp)).get(f"{args.workload}/gemv_kernel{info['gemv_kernel']}")
         if tj:
             traffic = tj.get("dram_bytes_per_launch")
     iter_bytes = gemv_bytes + 2 * 12.0 * nnz + 8.0 * (m + 1) + 8.0 * (n + 1) + 8.0 * 2 * m + 8.0 * 12 * n
@@ -274,9 +288,10 @@ def run_ours(args):
             "pcg_iters_per_qp": pcg_total / args.steps, "ipm_iters": ipm_iters, "status": statuses,
             "pcg_iter_us_isolated": pcg_iter_ms * 1e3,
             "op_apply_GBps": iter_bytes / (pcg_iter_ms * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "k_gemv_tiles<VEC,1> (PCG GEMV, p^T H p fused)",
+            "roofline": {"bound": "hbm", "kernel": kname,
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": gemv_bytes,
+                         "dense_equivalent_GBps": effective,
                          "launch_ms": gemv_ms, "peak_source": peak_src,
                          "timing": "CUDA events on the library stream, back-to-back launches after the timed region"},
             "cpu_baseline": cpu,
@@ -293,7 +308,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C3", choices=["C1", "C2", "C3", "C5"])
     ap.add_argument("--seed", type=int, default=0)

@@ -137,6 +137,16 @@ typedef struct {
     double obj;
 } ipm_trace_rec;
 
+/* Static facts about a created context (which kernels were selected, the partition). */
+typedef struct {
+    int32_t gemv_kernel;        /* 1 LDG tiles, 2 TMA-bulk, 3 symmetric upper-triangle TMA */
+    int32_t ncb;                /* column blocks of the GEMV tile-partial layout */
+    int32_t group_lanes;        /* lanes per A^T row in the fused SpMV^T kernels */
+    int32_t sharded;            /* 1 when the row-sharded code path is active */
+    int32_t rank, nranks;
+    int64_t row_begin, row_end; /* rows of H owned by this context */
+} ipm_info;
+
 /* Fill defaults (documented per field above). */
 void ipm_options_default(ipm_options *opt);
 
@@ -170,6 +180,7 @@ ipm_status ipm_get_solution(ipm_ctx *ctx, double *x, double *lam_lA, double *lam
                             double *lam_lx, double *lam_ux, double *obj_host);
 
 ipm_status ipm_get_stats(ipm_ctx *ctx, ipm_stats *stats);
+ipm_status ipm_get_info(const ipm_ctx *ctx, ipm_info *info);
 /* Copy up to cap trace records of the last solve (requires opt.trace = 1). */
 ipm_status ipm_get_trace(ipm_ctx *ctx, ipm_trace_rec *recs_host, int32_t cap, int32_t *count_host);
 

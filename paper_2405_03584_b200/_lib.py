@@ -54,6 +54,12 @@ class ipm_trace_rec(C.Structure):
                 ("obj", C.c_double)]
 
 
+class ipm_info(C.Structure):
+    _fields_ = [("gemv_kernel", C.c_int32), ("ncb", C.c_int32), ("group_lanes", C.c_int32),
+                ("sharded", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64)]
+
+
 _P = C.c_void_p
 _D = C.c_double
 _S = C.c_int32
@@ -68,6 +74,7 @@ _sigs = {
     "ipm_solve": ([_P], _S),
     "ipm_get_solution": ([_P, _P, _P, _P, _P, _P, C.POINTER(_D)], _S),
     "ipm_get_stats": ([_P, C.POINTER(ipm_stats)], _S),
+    "ipm_get_info": ([_P, C.POINTER(ipm_info)], _S),
     "ipm_get_trace": ([_P, C.POINTER(ipm_trace_rec), C.c_int32, C.POINTER(C.c_int32)], _S),
     "ipm_set_linear_term": ([_P, _P], _S),
     "ipm_update_hessian_rank2": ([_P, _P, _D, _P, _D], _S),

@@ -1051,6 +1051,19 @@ IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, doub
     return IPM_OK;
 }
 
+IPM_EXPORT ipm_status ipm_get_info(const ipm_ctx *ctx, ipm_info *info) {
+    if (!ctx || !info) return fail(nullptr, IPM_ERR_INVALID, "null argument");
+    info->gemv_kernel = ctx->P.gemv_sym ? 3 : (ctx->P.gemv_bulk ? 2 : 1);
+    info->ncb = ctx->ncb;
+    info->group_lanes = ctx->G;
+    info->sharded = ctx->sharded ? 1 : 0;
+    info->rank = ctx->comm ? ctx->comm->rank : 0;
+    info->nranks = ctx->comm ? ctx->comm->nranks : 1;
+    info->row_begin = ctx->row0;
+    info->row_end = ctx->row0 + ctx->nloc;
+    return IPM_OK;
+}
+
 IPM_EXPORT int64_t ipm_kernel_launches(const ipm_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
 IPM_EXPORT const char *ipm_last_error(const ipm_ctx *ctx) {

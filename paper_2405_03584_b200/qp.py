@@ -152,6 +152,11 @@ class QP:
         d["status"] = L.STATUS_NAMES.get(d["status"], d["status"])
         return d
 
+    def info(self) -> dict:
+        i = L.ipm_info()
+        L.check(L.ipm_get_info(self.ctx, C.byref(i)), self.ctx)
+        return {k: getattr(i, k) for k, _ in L.ipm_info._fields_}
+
     def trace(self) -> list:
         cnt = C.c_int32()
         L.check(L.ipm_get_trace(self.ctx, None, 0, C.byref(cnt)), self.ctx)
