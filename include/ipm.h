@@ -78,6 +78,8 @@ typedef struct {
     double warm_shift;          /* 1e-3   theta of the warm-start rule (R15) */
     int32_t gemv_kernel;        /* 0 auto (3 when H == H^T bitwise and unsharded, else 2), 1 LDG.128 register
                                    tiles, 2 TMA-bulk mbarrier pipeline, 3 symmetric upper-triangle TMA-bulk */
+    int32_t pcg_warm_start;     /* 0: each PCG starts from x0 = 0 (default, R11); 1: from the previous
+                                   search direction (S:248 option) */
 } ipm_options;
 
 /* Problem description for ipm_create.  Large arrays are BORROWED (the caller keeps them

@@ -135,6 +135,7 @@ struct ipm_ctx {
     bool have_iterate = false;   // V holds a valid iterate (after a solve or set_iterate)
     bool user_iterate = false;   // set_iterate called: next solve starts from it
     bool warm_pending = false;   // ipm_warm_start called
+    bool have_dx = false;        // V.dx holds a previous PCG solution (PCG warm start)
     double mu = 0.0;
     ipm_stats stats{};
     std::vector<ipm_trace_rec> trace;
@@ -142,6 +143,7 @@ struct ipm_ctx {
     int64_t launches = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     alignas(64) unsigned char tmap_sym[128] = {};   // CUtensorMap for the symmetric GEMV
+    ipm::Fork fork{nullptr, nullptr, nullptr};      // SpMV || GEMV branch of a PCG iteration
     // row-sharded mode
     ipm::Comm *comm = nullptr;
     bool sharded = false;
@@ -305,7 +307,8 @@ ipm_status build_graph(ipm_ctx *ctx) {
     CK(cudaGraphAddNode(&node, ctx->graph, nullptr, 0, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(ctx->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle, 1, ctx->cap);
+    launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle, 1, ctx->cap,
+                         &ctx->fork);
     cudaGraph_t captured = nullptr;
     CK(cudaStreamEndCapture(ctx->cap, &captured));
     CK(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
@@ -325,11 +328,21 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
     const Prob &P = ctx->P;
     Vecs &V = ctx->V;
     int64_t maxit = ctx->opt.pcg_max_iter > 0 ? ctx->opt.pcg_max_iter : 10 * (int64_t)ctx->n;
-    launch_pcg_init(P, V, ctx->sc, V.rhs, V.dx, rtol, ctx->opt.pcg_atol, maxit, ctx->st);
+    // warm start (option): x0 = the previous direction still held in V.dx
+    const int warm = (ctx->opt.pcg_warm_start && ctx->have_dx) ? 1 : 0;
+    launch_pcg_init(P, V, ctx->sc, V.rhs, V.dx, rtol, ctx->opt.pcg_atol, maxit, warm, ctx->st);
     DSYNC("pcg_init");
     ctx->launches += 1;
     CKL();
     TRY(xcombine(ctx, X_PCG_INIT, rtol, ctx->opt.pcg_atol, maxit));
+    if (warm) {
+        TRY(op_apply(ctx, V.dx, nullptr, V.pr, V.rhs, 1));      // r = rhs - K x0
+        launch_pcg_restart(P, V, ctx->sc, ctx->st);              // z, rho, rr, done
+        ctx->launches += 1;
+        CKL();
+        TRY(xcombine(ctx, X_PCG_RESTART));
+    }
+    ctx->have_dx = true;
     const bool graph = ctx->opt.use_graph && !ctx->sharded;
     if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
@@ -350,7 +363,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
             // host-driven fallback: batches of 16 iterations with device-side early exit
             for (;;) {
                 for (int b = 0; b < 16; ++b)
-                    launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st);
+                    launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork);
                 TRY(sync_scalars(ctx));
                 DBG("  host batch: it=%lld rr=%.3e done=%lld\n", (long long)ctx->hsc->it, ctx->hsc->rr, (long long)ctx->hsc->done);
                 ctx->launches += 16 * (3 + (P.m > 0 ? 1 : 0));
@@ -708,6 +721,9 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
     ipm_status s = IPM_OK;
         CK(cudaGetDevice(&ctx->device));
         CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->fork.side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->fork.ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->fork.ev_join, cudaEventDisableTiming));
         CK(cudaMallocHost(&ctx->hsc, sizeof(Scalars)));
         for (auto &e : ctx->ev) CK(cudaEventCreate(&e));
         // --- host validation of the O(n + m + nnz) data --------------------------------
@@ -1033,7 +1049,7 @@ IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, doub
         // what 0: the PCG GEMV's full work (tiles + fused p^T H p) without its done/alpha epilogue
         if (what == 0) launch_gemv(P, V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV_PCG, ctx->st);
         else if (what == 1) launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
-        else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st);
+        else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork);
     };
     one();  // warm-up
     CK(cudaEventRecord(ctx->ev[2], ctx->st));
@@ -1076,6 +1092,9 @@ IPM_EXPORT void ipm_destroy(ipm_ctx *ctx) {
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->graph) cudaGraphDestroy(ctx->graph);
     if (ctx->cap) cudaStreamDestroy(ctx->cap);
+    if (ctx->fork.side) cudaStreamDestroy(ctx->fork.side);
+    if (ctx->fork.ev_fork) cudaEventDestroy(ctx->fork.ev_fork);
+    if (ctx->fork.ev_join) cudaEventDestroy(ctx->fork.ev_join);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->hsc) cudaFreeHost(ctx->hsc);

@@ -45,9 +45,13 @@ void launch_rank2(const Prob &P, int row0, const double *u, double a, const doub
 
 // pcg.cu
 void launch_pcg_init(const Prob &P, const Vecs &V, Scalars *sc, const double *rhs, double *x, double rtol,
-                     double atol, int64_t maxit, cudaStream_t st);
+                     double atol, int64_t maxit, int keep_x, cudaStream_t st);
+struct Fork {  // side stream + events for the SpMV || GEMV branch of a PCG iteration
+    cudaStream_t side;
+    cudaEvent_t ev_fork, ev_join;
+};
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
-                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st);
+                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork);
 void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
 void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st);

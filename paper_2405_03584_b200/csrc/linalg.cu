@@ -113,17 +113,7 @@ k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
             sc->counters[cid] = 0;
             sc->S_H = tot;
             if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
-            if (MODE == 1 && !sc->sharded) {
-                const double pkp = tot + sc->S_b + sc->S_c;
-                sc->pKp = pkp;
-                if (!(pkp > 0.0) || !finite_d(pkp)) {
-                    sc->breakdown = 1;
-                    sc->done = 1;
-                    sc->alpha = 0.0;
-                } else {
-                    sc->alpha = sc->rho / pkp;
-                }
-            }
+            // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
     }
 }
@@ -299,17 +289,7 @@ k_gemv_bulk(const double *__restrict__ H, int64_t ldh, int nrows, int ncols, con
             sc->counters[cid] = 0;
             sc->S_H = tot;
             if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
-            if (MODE == 1 && !sc->sharded) {
-                const double pkp = tot + sc->S_b + sc->S_c;
-                sc->pKp = pkp;
-                if (!(pkp > 0.0) || !finite_d(pkp)) {
-                    sc->breakdown = 1;
-                    sc->done = 1;
-                    sc->alpha = 0.0;
-                } else {
-                    sc->alpha = sc->rho / pkp;
-                }
-            }
+            // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
     }
 }
@@ -544,7 +524,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
             sc->counters[cid] = 0;
             sc->S_H = tot;
             if (sc->sharded) sc->loc[1] = tot;
-            if (MODE == 1 && !sc->sharded) fin_pcg_alpha(sc, tot + sc->S_b + sc->S_c);
+            // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
     }
 }

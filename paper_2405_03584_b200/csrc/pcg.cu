@@ -45,13 +45,13 @@ static int grid_for(int64_t units, int per_block) {
 __global__ void __launch_bounds__(kBlock)
 k_pcg_init(int n, const double *__restrict__ rhs, double *__restrict__ x, double *__restrict__ r,
            double *__restrict__ z, const double *__restrict__ Minv, double *__restrict__ p1,
-           double *__restrict__ p2, double *__restrict__ p3, Scalars *sc, double rtol, double atol, int64_t maxit) {
+           double *__restrict__ p2, int keep_x, Scalars *sc, double rtol, double atol, int64_t maxit) {
     __shared__ double red[kBlock / 32];
     double rz = 0.0, rr = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const double ri = rhs[i];
         const double zi = Minv[i] * ri;
-        x[i] = 0.0;
+        if (!keep_x) x[i] = 0.0;        // keep_x: warm start, r is replaced by rhs - K x next
         r[i] = ri;
         z[i] = zi;
         rz = fma(ri, zi, rz);
@@ -76,13 +76,12 @@ k_pcg_init(int n, const double *__restrict__ rhs, double *__restrict__ x, double
             }
         }
     }
-    (void)p3;
 }
 
 void launch_pcg_init(const Prob &P, const Vecs &V, Scalars *sc, const double *rhs, double *x, double rtol,
-                     double atol, int64_t maxit, cudaStream_t st) {
+                     double atol, int64_t maxit, int keep_x, cudaStream_t st) {
     const int grid = grid_for(P.n, kBlock);
-    k_pcg_init<<<grid, kBlock, 0, st>>>(P.n, rhs, x, V.pr, V.pz, V.Minv, V.part[0], V.part[1], V.part[2], sc, rtol,
+    k_pcg_init<<<grid, kBlock, 0, st>>>(P.n, rhs, x, V.pr, V.pz, V.Minv, V.part[0], V.part[1], keep_x, sc, rtol,
                                         atol, maxit);
 }
 
@@ -182,7 +181,27 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
         return;
     }
-    const double alpha = sc->alpha;
+    // alpha = rho / p^T K p with p^T K p = S_H (GEMV) + S_b (k_pcg_p) + S_c (SpMV): the SpMV and
+    // the GEMV run concurrently, so the three partial sums meet here; every block evaluates the
+    // same expression (bitwise identical), block 0 publishes it.  Sharded: k_xcombine did it.
+    double alpha;
+    if (sc->sharded) {
+        alpha = sc->alpha;
+    } else {
+        const double pkp = sc->S_H + sc->S_b + sc->S_c;
+        if (!(pkp > 0.0) || !finite_d(pkp)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                fin_pcg_alpha(sc, pkp);      // breakdown: done = 1
+                if (use_cond) cudaGraphSetConditional(h, 0);
+            }
+            return;
+        }
+        alpha = sc->rho / pkp;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->pKp = pkp;
+            sc->alpha = alpha;
+        }
+    }
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
     double rz = 0.0, rr = 0.0;
@@ -251,14 +270,25 @@ void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc
 }
 
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
-                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
+                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork) {
     const int grid = grid_for(P.n, kBlock);
     k_pcg_p<<<grid, kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2], sc);
     if (!use_cond) dstage("pcg_p", st);
-    launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
-    if (!use_cond) dstage("spmv", st);
+    // t = Sigma_c o (A p) only shares p with the GEMV: run it on a side stream (a parallel
+    // branch of the captured graph) next to the HBM-bound GEMV; joined before the update.
+    const bool par = fork != nullptr && P.m > 0;
+    if (par) {
+        cudaEventRecord(fork->ev_fork, st);
+        cudaStreamWaitEvent(fork->side, fork->ev_fork, 0);
+        launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, fork->side);
+        cudaEventRecord(fork->ev_join, fork->side);
+    } else {
+        launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
+        if (!use_cond) dstage("spmv", st);
+    }
     launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);
     if (!use_cond) dstage("gemv", st);
+    if (par) cudaStreamWaitEvent(st, fork->ev_join, 0);
     const int ug = grid_for(P.n, kBlock / G);
     const double *t = (P.m > 0) ? V.pt : nullptr;
 #define IPM_UPD(GG)                                                                                              \

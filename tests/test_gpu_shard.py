@@ -40,9 +40,9 @@ def test_sharded_p1_is_bitwise_the_unsharded_path():
     one-GPU path bit for bit (the combine applies the same epilogue in the same order)."""
     from paper_2405_03584_b200 import QP
     q = planted_qp(900, 250, density=0.03, rank=32, seed=8, rows="mixed", var="mixed")
-    a = QP(device=DEV, **problem_tensors(q, DEV))
+    a = QP(device=DEV, gemv_kernel=2, **problem_tensors(q, DEV))   # the sharded path's GEMV
     a.solve()
-    grp, qps = _sharded(q, 1)
+    grp, qps = _sharded(q, 1, gemv_kernel=2)
     st, x, stats = _solve_all(grp, qps)
     assert st == ["ok"]
     assert np.array_equal(a.solution()["x"].cpu().numpy(), x)
