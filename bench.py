@@ -9,8 +9,8 @@ patient-case-shaped QP (n=20000, m=5000, 1% dense A, dense 3.2 GB H) — see DES
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl ours|reference]
 
 value = QPs solved per second over the whole job (all ranks) = N*K / max-over-ranks time.
-N > 1 runs independent replicas (one QP per rank; "scaling": "weak") until the row-sharded
-C5 path is wired into the bench.  --impl reference times the CPU oracle (oracle/) as it
+N > 1 solves ONE QP row-sharded over the N GPUs (NCCL allgathers inside libipm; "scaling":
+"strong"); --replicas runs N independent QPs instead ("weak").  --impl reference times the CPU oracle (oracle/) as it
 stands on the host cores, on a bounded sample (one IPM iteration per step) scaled to QP/s.
 """
 from __future__ import annotations
@@ -152,7 +152,7 @@ def run_reference(args):
               f"QP time = {t_iter:.2f} s/iter x {n_ipm} IPM iterations [{src}]")
     line = {"impl": "reference", "metric": METRIC, "value": 1.0 / qp_s, "unit": "QP/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": qp_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/planted.py, seeded)",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/planted.py, seeded)",
             "config": {"workload": args.workload, "seed": args.seed},
             "cpu_baseline": {"value": 1.0 / qp_s, "unit": "QP/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": 1.0 / qp_s, "unit": "QP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -176,9 +176,28 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     q = config(args.workload, args.seed)
     n, m, nnz = q.n, q.m, q.nnz
-    t = problem_tensors(q, dev)
+    # N > 1: ONE QP row-sharded over the ranks (NCCL allgathers inside libipm),
+    # each rank building only its row block of H on its device; --replicas: N independent QPs.
+    sharded = (ws > 1 or args.force_shard) and not args.replicas
+    rows = (0, n)
+    if sharded:
+        from gen.torch_io import device_hessian
+        from paper_2405_03584_b200.dist import broadcast_unique_id, nccl_shard, nccl_unique_id, partition
+        rows = partition(n, ws)[rank]
+        Hb, ldh = device_hessian(q, dev, rows=rows)
+        t = problem_tensors(q, dev, H=Hb, ldh=ldh)
+
+        def make_qp(tensors):
+            uid = (nccl_unique_id() if ws == 1
+                   else broadcast_unique_id(nccl_unique_id, rank, dist.broadcast_object_list))
+            return QP(device=dev, shard=nccl_shard(rank, ws, uid), **tensors)
+    else:
+        t = problem_tensors(q, dev)
+
+        def make_qp(tensors):
+            return QP(device=dev, **tensors)
     torch.cuda.synchronize()
-    qp = QP(device=dev, **t)
+    qp = make_qp(t)
     stream = qp.stream
 
     def barrier():
@@ -229,12 +248,13 @@ def run_ours(args):
         gemv_bytes = 8.0 * tri + 8.0 * n + 8.0 * n * ncb
         kname = "k_symv_bulk<1> (symmetric upper-triangle GEMV, 2-D TMA, p^T H p fused)"
     else:
-        gemv_bytes = 8.0 * n * n + 8.0 * n + 8.0 * n * ncb   # H + p + tile partials
+        nrow = rows[1] - rows[0]
+        gemv_bytes = 8.0 * nrow * n + 8.0 * n + 8.0 * nrow * ncb   # H (local rows) + p + tile partials
         kname = ("k_gemv_bulk<1> (TMA-bulk GEMV, p^T H p fused)" if info["gemv_kernel"] == 2
                  else "k_gemv_tiles<1,1> (LDG.128 GEMV, p^T H p fused)")
     peak, peak_src = _peaks()
     achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
-    effective = 8.0 * n * n / (gemv_ms * 1e-3) / 1e9          # dense-H-equivalent rate
+    effective = 8.0 * (rows[1] - rows[0]) * n / (gemv_ms * 1e-3) / 1e9   # dense-H-equivalent rate
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemv_traffic.json")
     if os.path.exists(tp):
@@ -244,13 +264,21 @@ def run_ours(args):
     iter_bytes = gemv_bytes + 2 * 12.0 * nnz + 8.0 * (m + 1) + 8.0 * (n + 1) + 8.0 * 2 * m + 8.0 * 12 * n
 
     # --- end to end through the public API with host buffers ----------------------------
-    th = problem_tensors(q, dev, host=True)
+    if sharded:
+        import numpy as np
+        from gen.planted import hessian_rows
+        ldh_h = n + (n & 1)
+        Hh = np.zeros((rows[1] - rows[0], ldh_h))
+        Hh[:, :n] = hessian_rows(q.d, q.U, q.w, rows[0], rows[1])
+        th = problem_tensors(q, dev, H=torch.from_numpy(Hh).pin_memory(), ldh=ldh_h, host=True)
+    else:
+        th = problem_tensors(q, dev, host=True)
     h2d = sum(v.numel() * v.element_size() for k, v in th.items() if hasattr(v, "numel"))
     e2e_times = []
     for _ in range(args.steps):
         torch.cuda.synchronize()
         a0 = time.perf_counter()
-        qp2 = QP(device=dev, **th)            # H2D of every input (pinned), validation, A^T build
+        qp2 = make_qp(th)                     # H2D of every input (pinned), validation, A^T build
         qp2.solve()
         x_host = qp2.solution()["x"].cpu()   # D2H of the result
         torch.cuda.synchronize()
@@ -261,7 +289,7 @@ def run_ours(args):
     te = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    d2h = n * 8
+    d2h = (rows[1] - rows[0]) * 8
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -274,15 +302,16 @@ def run_ours(args):
                          f"of K on {cores} host threads) x {n_ipm} IPM iterations [{src}]"}
 
     if rank == 0:
-        qps = ws * args.steps / t_max
+        qps = (1 if sharded else ws) * args.steps / t_max
         line = {
             "metric": METRIC, "value": qps, "unit": "QP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic planted-KKT QP (gen/planted.py, seeded; random-init dyadic H = diag + U W U^T)",
             "config": {"workload": args.workload, **CONFIGS[args.workload], "seed": args.seed, "nnz": nnz,
                        "H_bytes": 8 * n * n, "l2": "inputs larger than L2 (H >> 126 MB), no flush",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+                       "parallelism": (f"row-sharded H over {ws} GPUs (NCCL allgather)" if sharded
+                                       else (f"replicas x{ws}" if ws > 1 else "1 GPU"))},
             "qp_solve_s": t_max / args.steps,
             "pcg_it_per_s": pcg_total / (pcg_ms * 1e-3) if pcg_ms > 0 else None,
             "pcg_iters_per_qp": pcg_total / args.steps, "ipm_iters": ipm_iters, "status": statuses,
@@ -295,7 +324,8 @@ def run_ours(args):
                          "launch_ms": gemv_ms, "peak_source": peak_src,
                          "timing": "CUDA events on the library stream, back-to-back launches after the timed region"},
             "cpu_baseline": cpu,
-            "e2e": {"value": ws * args.steps / float(te.item()), "unit": "QP/s", "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": (1 if sharded else ws) * args.steps / float(te.item()), "unit": "QP/s",
+                    "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches), "clocks": clk,
         }
@@ -314,6 +344,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: N independent QPs instead of one sharded QP")
+    ap.add_argument("--force-shard", action="store_true", help="N=1: run the NCCL row-sharded code path")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

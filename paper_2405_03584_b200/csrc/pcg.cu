@@ -209,6 +209,15 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
     for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
         const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
         const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
+        // lane 0's row operands are independent of the reduction: load them first
+        double pi = 0.0, sbi = 0.0, xi = 0.0, ri0 = 0.0, mi = 0.0;
+        if (gl == 0) {
+            pi = p[i];
+            sbi = sigb[i];
+            xi = x[i];
+            ri0 = r[i];
+            mi = Minv[i];
+        }
         double s = 0.0;
         for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
         if (t != nullptr) {
@@ -217,12 +226,11 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
         }
         s = group_sum<G>(s);
         if (act && gl == 0) {
-            const double pi = p[i];
-            const double yi = fma(sigb[i], pi, s);
-            x[i] = fma(alpha, pi, x[i]);
-            const double ri = fma(-alpha, yi, r[i]);
+            const double yi = fma(sbi, pi, s);
+            x[i] = fma(alpha, pi, xi);
+            const double ri = fma(-alpha, yi, ri0);
             r[i] = ri;
-            const double zi = Minv[i] * ri;
+            const double zi = mi * ri;
             z[i] = zi;
             rz = fma(ri, zi, rz);
             rr = fma(ri, ri, rr);

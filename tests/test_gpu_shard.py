@@ -50,6 +50,21 @@ def test_sharded_p1_is_bitwise_the_unsharded_path():
     assert stats[0]["pcg_iters_total"] == a.stats()["pcg_iters_total"]
 
 
+def test_nccl_transport_single_rank():
+    """The NCCL backend (dlopen'd libnccl, ncclCommInitRank, ncclAllGather) with one rank runs
+    the sharded path and reproduces the unsharded solve bitwise."""
+    from paper_2405_03584_b200 import QP
+    from paper_2405_03584_b200.dist import nccl_shard, nccl_unique_id
+    q = config("C1", 2)
+    t = problem_tensors(q, DEV)
+    a = QP(device=DEV, gemv_kernel=2, **t)
+    a.solve()
+    b = QP(device=DEV, gemv_kernel=2, shard=nccl_shard(0, 1, nccl_unique_id()), **t)
+    assert b.info()["sharded"] == 1
+    assert b.solve() == "ok"
+    assert torch.equal(a.solution()["x"], b.solution()["x"])
+
+
 @pytest.mark.parametrize("P", [2, 3, 4])
 def test_sharded_matches_oracle(P):
     q = planted_qp(1001, 300, density=0.02, rank=32, seed=40 + P, rows="vmat", var="box")
