@@ -138,8 +138,8 @@ def run_reference(args):
         return
     n_ipm, src = oracle_ipm_iters(args.workload, args.seed)
     times = []
-    for _ in range(args.warmup if args.warmup < 1 else 0):
-        pass
+    for _ in range(args.warmup):          # untimed warm-up samples (page-in, BLAS thread pools)
+        oracle_sample(args.workload, args.seed, 1)
     cores = None
     for k in range(args.steps):
         dt, cores = oracle_sample(args.workload, args.seed, 1)
@@ -152,7 +152,7 @@ def run_reference(args):
               f"QP time = {t_iter:.2f} s/iter x {n_ipm} IPM iterations [{src}]")
     line = {"impl": "reference", "metric": METRIC, "value": 1.0 / qp_s, "unit": "QP/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": qp_s * 1e3, "higher_is_better": True,
-            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/planted.py, seeded)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/planted.py, seeded)",
             "config": {"workload": args.workload, "seed": args.seed},
             "cpu_baseline": {"value": 1.0 / qp_s, "unit": "QP/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": 1.0 / qp_s, "unit": "QP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -291,6 +291,24 @@ def run_ours(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     d2h = (rows[1] - rows[0]) * 8
 
+    # --- the smaller configs of BASELINE.json, for context (median QP time, 1 GPU) ----------
+    others = {}
+    if ws == 1 and not args.no_extra:
+        for wl, reps in (("C1", 5), ("C2", 3)):
+            qo = config(wl, args.seed)
+            qx = QP(device=dev, **problem_tensors(qo, dev))
+            qx.solve()
+            ts = []
+            for _ in range(reps):
+                qx.solve()
+                ts.append(qx.stats())
+            ts.sort(key=lambda s: s["t_solve_ms"])
+            med = ts[len(ts) // 2]
+            others[wl] = {"qp_solve_ms": med["t_solve_ms"], "ipm_iters": med["ipm_iters"],
+                          "pcg_iters": med["pcg_iters_total"], "status": med["status"],
+                          "gemv_kernel": qx.info()["gemv_kernel"]}
+            qx.close()
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         n_ipm, src = oracle_ipm_iters(args.workload, args.seed)
@@ -327,7 +345,7 @@ def run_ours(args):
             "e2e": {"value": (1 if sharded else ws) * args.steps / float(te.item()), "unit": "QP/s",
                     "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
-            "gpu_launches": int(launches), "clocks": clk,
+            "gpu_launches": int(launches), "clocks": clk, "other_workloads": others,
         }
         print(json.dumps(line), flush=True)
     qp.close()
@@ -346,6 +364,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: N independent QPs instead of one sharded QP")
     ap.add_argument("--force-shard", action="store_true", help="N=1: run the NCCL row-sharded code path")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C1/C2 context timings")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -334,10 +334,16 @@ void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double
 // the persistent CTAs as contiguous ranges.
 constexpr int kSymSR = 32;
 constexpr int kSymStages = 3;
-constexpr int kSymRW = kSymSR / kBulkConsumers;   // strip rows reduced by each consumer warp
+constexpr int kSymConsumers = 16;                 // consumer warps (2 per strip row pair)
+constexpr int kSymThreads = 32 * (kSymConsumers + 1);
+constexpr int kSymRW = kSymSR / kSymConsumers;    // strip rows reduced by each consumer warp
 constexpr int kSymStageDoubles = kSymSR * kSymB + kSymB + kSymSR;
 constexpr size_t kSymSmem = (size_t)kSymStages * kSymStageDoubles * 8 + 2 * kSymStages * 8;
-static_assert(kBulkConsumers * 32 == kSymB, "one consumer thread per tile column");
+static_assert(kSymConsumers * 32 == 2 * kSymB, "two consumer threads (row halves) per tile column");
+
+__device__ __forceinline__ void consumers_sync() {      // named barrier 1: consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(kSymConsumers * 32) : "memory");
+}
 
 __device__ __forceinline__ void sym_locate(int64_t t, int nb, int &I, int &J) {
     int i = 0;
@@ -382,12 +388,13 @@ bool make_sym_tensor_map(const Prob &P, void *out) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kBulkThreads, 1)
+__global__ void __launch_bounds__(kSymThreads, 1)
 k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__restrict__ p,
             const double *__restrict__ pdot, double *__restrict__ ypart, int nb, double *__restrict__ dpart,
             Scalars *sc, int cid) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ double red[kBulkThreads / 32];
+    __shared__ double red[kSymThreads / 32];
+    __shared__ double colbuf[kSymB];                  // row-half-1 column sums of the current tile
     if (MODE == 1 && sc->done) return;
     double *stages = reinterpret_cast<double *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kSymStages * kSymStageDoubles * 8);
@@ -396,7 +403,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
     if (threadIdx.x == 0) {
         for (int s = 0; s < kSymStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kBulkConsumers);
+            mbar_init(&empty[s], kSymConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -407,7 +414,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
     double dacc = 0.0;
     int I = 0, J = 0;
     if (t0 < t1) sym_locate(t0, nb, I, J);
-    if (warp == kBulkConsumers) {
+    if (warp == kSymConsumers) {
         if (lane == 0) {
             uint64_t pol_h, pol_p;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_h));
@@ -438,17 +445,19 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
         __syncwarp();
     } else {
         // Latency matters more than bandwidth here (2 KB rows): every operand comes from the
-        // stage in shared memory (including the p entries of the fused p^T H p), the two rows
-        // of a warp share one interleaved shuffle tree, and the column sums use two chains.
-        const int c = threadIdx.x;            // tile column owned by this thread
+        // stage in shared memory (including the p entries of the fused p^T H p); warp w reduces
+        // strip rows w and w + 16 with interleaved shuffle trees; thread t owns tile column
+        // c = t mod 256 for strip rows of half h = t / 256 (two chains), and the two halves are
+        // added in fixed order through shared memory at the end of the tile.
+        const int c = threadIdx.x & (kSymB - 1);
+        const int h = threadIdx.x / kSymB;
         int stage = 0;
         uint32_t phase = 0;
         for (int64_t t = t0; t < t1; ++t) {
             const int rowsI = min(kSymB, n - I * kSymB);
             const int colsJ = min(kSymB, n - J * kSymB);
             const bool diag = (I == J);
-            double cacc[4] = {0.0, 0.0, 0.0, 0.0};
-            double pj_c = 0.0;
+            double ce = 0.0, co = 0.0, pj_c = 0.0;
             for (int s0 = 0; s0 < rowsI; s0 += kSymSR) {
                 const int rows = min(kSymSR, rowsI - s0);
                 mbar_wait(&full[stage], phase);
@@ -456,7 +465,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                 const double *sPJ = sH + kSymSR * kSymB;
                 const double *sPI = sPJ + kSymB;
                 if (s0 == 0 && c < colsJ) pj_c = sPJ[c];
-                // row part: rows warp + 8 k (k < kSymRW) of the strip (OOB rows are zero-filled)
+                // row part: rows warp + 16 q (q < kSymRW) of the strip (OOB rows are zero-filled)
                 const double2 *pv = reinterpret_cast<const double2 *>(sPJ);
                 double a[kSymRW], b[kSymRW];
 #pragma unroll
@@ -467,7 +476,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                         const double2 pk = pv[k];
 #pragma unroll
                         for (int q = 0; q < kSymRW; ++q) {
-                            const double2 x = reinterpret_cast<const double2 *>(sH + (warp + q * kBulkConsumers) * kSymB)[k];
+                            const double2 x = reinterpret_cast<const double2 *>(sH + (warp + q * kSymConsumers) * kSymB)[k];
                             a[q] = fma(x.x, pk.x, a[q]);
                             b[q] = fma(x.y, pk.y, b[q]);
                         }
@@ -476,7 +485,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                 if ((colsJ & 1) && lane == 0) {
 #pragma unroll
                     for (int q = 0; q < kSymRW; ++q)
-                        a[q] = fma(sH[(warp + q * kBulkConsumers) * kSymB + colsJ - 1], sPJ[colsJ - 1], a[q]);
+                        a[q] = fma(sH[(warp + q * kSymConsumers) * kSymB + colsJ - 1], sPJ[colsJ - 1], a[q]);
                 }
                 double s[kSymRW];
 #pragma unroll
@@ -490,27 +499,36 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                     const int row = I * kSymB + s0;
 #pragma unroll
                     for (int q = 0; q < kSymRW; ++q) {
-                        const int r = warp + q * kBulkConsumers;
+                        const int r = warp + q * kSymConsumers;
                         if (r < rows) {
                             ypart[(int64_t)(row + r) * nb + J] = s[q];
                             if (pdot) dacc = fma(sPI[r], s[q], dacc);
                         }
                     }
                 }
-                // column part (H_IJ^T p_I) for this thread's column: four interleaved chains
+                // column part (H_IJ^T p_I): this thread's column over its half of the strip rows
                 if (!diag && c < colsJ) {
+                    const int rb0 = h * (kSymSR / 2);
 #pragma unroll
-                    for (int r = 0; r < kSymSR; ++r)
-                        if (r < rows) cacc[r & 3] = fma(sH[r * kSymB + c], sPI[r], cacc[r & 3]);
+                    for (int r = 0; r < kSymSR / 2; r += 2) {
+                        if (rb0 + r < rows) ce = fma(sH[(rb0 + r) * kSymB + c], sPI[rb0 + r], ce);
+                        if (rb0 + r + 1 < rows) co = fma(sH[(rb0 + r + 1) * kSymB + c], sPI[rb0 + r + 1], co);
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
                 if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
             }
-            if (!diag && c < colsJ) {
-                const double colacc = (cacc[0] + cacc[1]) + (cacc[2] + cacc[3]);
-                ypart[(int64_t)(J * kSymB + c) * nb + I] = colacc;
-                if (pdot) dacc = fma(pj_c, colacc, dacc);
+            if (!diag) {                       // uniform over the consumer warps
+                const double part = ce + co;
+                if (h == 1 && c < colsJ) colbuf[c] = part;
+                consumers_sync();
+                if (h == 0 && c < colsJ) {
+                    const double colacc = part + colbuf[c];
+                    ypart[(int64_t)(J * kSymB + c) * nb + I] = colacc;
+                    if (pdot) dacc = fma(pj_c, colacc, dacc);
+                }
+                consumers_sync();
             }
             if (++J == nb) { ++I; J = I; }
         }
@@ -540,9 +558,9 @@ void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double
     const int nb = sym_ncb(P.n);
     const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(P.tmap_sym);
     if (mode == 1)
-        k_symv_bulk<1><<<grid, kBulkThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+        k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
     else
-        k_symv_bulk<0><<<grid, kBulkThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+        k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
 }
 
 // Exact-symmetry check at create (the symmetric GEMV is only used when H == H^T bitwise).
