@@ -216,6 +216,29 @@ def test_ipm_no_bounds_one_step():
     assert np.max(np.abs(x - xcf)) <= 1e-9 * np.max(np.abs(xcf))
 
 
+def test_ipm_vmat_ratio_more_rows_than_variables():
+    """VMAT H&N has ~5 linear constraints per variable (Table 1): m > n."""
+    q = planted_qp(300, 1500, density=0.05, rank=32, seed=13, rows="vmat", var="box")
+    _check_against_oracle(q)
+
+
+def test_ipm_empty_rows_and_single_variable():
+    q = planted_qp(40, 12, density=0.1, rank=8, seed=3, rows="mixed", var="mixed")
+    # empty the CSR rows 2 and 7 (their bounds stay valid: 0 in [l, u] is not required,
+    # an empty row is a constant 0 <= u or l <= 0 constraint -> drop its bounds)
+    keep = np.ones(q.nnz, bool)
+    for i in (2, 7):
+        keep[q.A_rowptr[i]:q.A_rowptr[i + 1]] = False
+        q.l[i], q.u[i] = -np.inf, np.inf
+    lens = np.diff(q.A_rowptr).copy()
+    lens[[2, 7]] = 0
+    q.A_col, q.A_val = q.A_col[keep], q.A_val[keep]
+    q.A_rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    _check_against_oracle(q, ftol=1e-8)
+    q1 = planted_qp(1, 1, density=1.0, rank=1, seed=2, rows="upper", var="box")
+    _check_against_oracle(q1)
+
+
 def test_ipm_deterministic_bitwise():
     q = planted_qp(900, 300, density=0.03, rank=32, seed=5, rows="mixed", var="mixed")
     qp = _qp(q, trace=1)
