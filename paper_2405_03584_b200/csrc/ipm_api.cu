@@ -343,12 +343,17 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
         TRY(xcombine(ctx, X_PCG_RESTART));
     }
     ctx->have_dx = true;
-    const bool graph = ctx->opt.use_graph && !ctx->sharded;
+    const bool small = !ctx->sharded && P.n <= kSmallN && ctx->opt.use_graph;
+    const bool graph = ctx->opt.use_graph && !ctx->sharded && !small;
     if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
     int64_t it_prev = 0;
     for (int round = 0;; ++round) {
-        if (graph) {
+        if (small) {
+            launch_pcg_small(P, V, ctx->sc, V.dx, ctx->st);
+            ctx->launches += 1;
+            TRY(sync_scalars(ctx));
+        } else if (graph) {
             CK(cudaGraphLaunch(ctx->gexec, ctx->st));
             TRY(sync_scalars(ctx));
         } else if (ctx->sharded) {

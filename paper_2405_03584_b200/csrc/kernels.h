@@ -54,6 +54,8 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
                           cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork);
 void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+constexpr int kSmallN = 256;        // single-CTA PCG loop below this size (launch-latency bound)
+void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cudaStream_t st);
 void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st);
 
 // shard.cu

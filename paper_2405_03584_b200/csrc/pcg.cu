@@ -258,6 +258,97 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
     }
 }
 
+// ------------------------------------------------------------- tiny problems: one CTA
+// For n <= kSmallN the four-kernel iteration is launch-latency bound (C1: ~23 us per
+// iteration for ~1 us of work), so the whole PCG loop runs inside ONE 512-thread CTA:
+// phases separated by __syncthreads, all reductions fixed-order block reductions.  Same
+// recurrence, same stopping rule and scalars as the multi-kernel path.
+__global__ void __launch_bounds__(512)
+k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_t *__restrict__ Arp,
+            const int *__restrict__ Acol, const double *__restrict__ Aval, const int64_t *__restrict__ ATrp,
+            const int *__restrict__ ATcol, const double *__restrict__ ATval, const double *__restrict__ sigb,
+            const double *__restrict__ sigc, const double *__restrict__ Minv, double *x, double *r, double *z,
+            double *p, double *t, double *y, Scalars *sc) {
+    __shared__ double red[32];
+    if (sc->done) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    double rho = sc->rho, rho_old = sc->rho_old, rr = sc->rr, pkp = 0.0;
+    int64_t it = sc->it, it_rs = sc->it_rs;
+    const double tol2 = sc->tol2;
+    const int64_t maxit = sc->maxit;
+    int breakdown = 0;
+    for (;;) {
+        const bool first = (it_rs == 0);
+        const double beta = first ? 0.0 : rho / rho_old;
+        for (int i = tid; i < n; i += blockDim.x) p[i] = first ? z[i] : fma(beta, p[i], z[i]);
+        __syncthreads();
+        for (int i = warp; i < m; i += nw) {                      // t = sig_c o (A p)
+            double a = 0.0;
+            for (int64_t k = Arp[i] + lane; k < Arp[i + 1]; k += 32) a = fma(Aval[k], p[Acol[k]], a);
+            a = warp_sum(a);
+            if (lane == 0) t[i] = sigc[i] * a;
+        }
+        __syncthreads();
+        double part = 0.0;
+        for (int i = warp; i < n; i += nw) {                      // y = H p + sig_b p + A^T t
+            double a = 0.0;
+            const double *h = H + (int64_t)i * ldh;
+            for (int j = lane; j < n; j += 32) a = fma(h[j], p[j], a);
+            if (m > 0)
+                for (int64_t k = ATrp[i] + lane; k < ATrp[i + 1]; k += 32) a = fma(ATval[k], t[ATcol[k]], a);
+            a = warp_sum(a);
+            if (lane == 0) {
+                const double yi = fma(sigb[i], p[i], a);
+                y[i] = yi;
+                part = fma(p[i], yi, part);
+            }
+        }
+        pkp = block_sum(part, red);
+        if (!(pkp > 0.0) || !finite_d(pkp)) {
+            breakdown = 1;
+            break;
+        }
+        const double alpha = rho / pkp;
+        double rz = 0.0, r2 = 0.0;
+        for (int i = tid; i < n; i += blockDim.x) {
+            x[i] = fma(alpha, p[i], x[i]);
+            const double ri = fma(-alpha, y[i], r[i]);
+            r[i] = ri;
+            const double zi = Minv[i] * ri;
+            z[i] = zi;
+            rz = fma(ri, zi, rz);
+            r2 = fma(ri, ri, r2);
+        }
+        rz = block_sum(rz, red);
+        r2 = block_sum(r2, red);
+        rho_old = rho;
+        rho = rz;
+        rr = r2;
+        ++it;
+        ++it_rs;
+        if (!finite_d(rr) || !finite_d(rho)) {
+            breakdown = 1;
+            break;
+        }
+        if (rr <= tol2 || it >= maxit) break;
+    }
+    if (tid == 0) {
+        sc->rho = rho;
+        sc->rho_old = rho_old;
+        sc->rr = rr;
+        sc->pKp = pkp;
+        sc->it = it;
+        sc->it_rs = it_rs;
+        sc->done = 1;
+        if (breakdown) sc->breakdown = 1;
+    }
+}
+
+void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cudaStream_t st) {
+    k_pcg_small<<<1, 512, 0, st>>>(P.n, P.m, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol, P.ATval, V.sig_b,
+                                    V.sig_c, V.Minv, x, V.pr, V.pz, V.pp, V.pt, V.py, sc);
+}
+
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
     k_pcg_p<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2], sc);
 }

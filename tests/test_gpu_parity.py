@@ -251,12 +251,31 @@ def test_ipm_deterministic_bitwise():
 
 
 def test_host_loop_fallback_equals_graph():
-    q = config("C1", 3)
+    """The CUDA-graph PCG (device WHILE node) and the host-driven loop launch the same kernels
+    in the same order: bitwise identical (n > 256, so the single-CTA path is not used)."""
+    q = planted_qp(700, 150, density=0.03, rank=32, seed=12, rows="mixed", var="mixed")
     a = _qp(q, use_graph=1)
     b = _qp(q, use_graph=0)
     a.solve()
     b.solve()
     assert torch.equal(a.solution()["x"], b.solution()["x"])
+
+
+def test_single_cta_pcg_small_n():
+    """n <= 256: the whole PCG loop in one CTA (launch-latency path) agrees with the
+    multi-kernel host loop to rounding and with the oracle."""
+    q = config("C1", 6)
+    a = _qp(q)               # single-CTA PCG
+    b = _qp(q, use_graph=0)  # multi-kernel loop
+    assert a.solve() == "ok" and b.solve() == "ok"
+    xa, xb = a.solution()["x"].cpu().numpy(), b.solution()["x"].cpu().numpy()
+    assert np.max(np.abs(xa - xb)) <= 1e-9 * max(1.0, np.max(np.abs(xb)))
+    assert abs(a.stats()["ipm_iters"] - b.stats()["ipm_iters"]) <= 1
+    sb, sc, _ = _rand_sigmas(q, 9)
+    K = okkt.condensed_matrix(q.H, q.A_dense(), sb, sc)
+    rhs = np.random.default_rng(2).normal(size=q.n)
+    x, it = a.pcg(sb, sc, rhs, 1e-11)
+    assert np.linalg.norm(rhs - K @ x.cpu().numpy()) <= 1.0000001e-11 * np.linalg.norm(rhs)
 
 
 # ---------------------------------------------------------------- validation / errors
