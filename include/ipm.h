@@ -111,6 +111,18 @@ typedef struct {
     int32_t rank, nranks;
     int32_t comm_kind;
     const void *comm_handle_host;
+    /* Hessian representation.  hess_kind 0: the dense H above.  hess_kind 1:
+     * compact quasi-Newton H = diag(h0) + U diag(w) U^T (eq:bfgs_hessian), applied
+     * matrix-free as h0 o p + U (w o (U^T p)); H and ldh are ignored.  U is BORROWED,
+     * n x ldu row-major, the first k columns in use; ipm_update_hessian_rank2 APPENDS (u, v) as
+     * columns k, k+1 with weights (alpha, beta) — the paper's SQP adds two columns per iteration
+     * — while k + 2 <= ldu.  h0 (n) and w (k) are copied.  Unsharded only. */
+    int32_t hess_kind;
+    int32_t k;
+    int64_t ldu;
+    const double *h0;
+    double *U;
+    const double *w;
 } ipm_problem;
 
 typedef struct ipm_group ipm_group;  /* in-process rank group (comm_kind 2) */

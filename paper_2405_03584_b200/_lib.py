@@ -38,7 +38,9 @@ class ipm_problem(C.Structure):
                 ("g", C.c_void_p), ("A_rowptr", C.c_void_p), ("A_col", C.c_void_p), ("A_val", C.c_void_p),
                 ("l", C.c_void_p), ("u", C.c_void_p), ("xl", C.c_void_p), ("xu", C.c_void_p),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("comm_kind", C.c_int32), ("comm_handle_host", C.c_void_p)]
+                ("comm_kind", C.c_int32), ("comm_handle_host", C.c_void_p),
+                ("hess_kind", C.c_int32), ("k", C.c_int32), ("ldu", C.c_int64), ("h0", C.c_void_p),
+                ("U", C.c_void_p), ("w", C.c_void_p)]
 
 
 class ipm_stats(C.Structure):

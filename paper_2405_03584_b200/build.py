@@ -15,7 +15,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["linalg.cu", "pcg.cu", "ipmops.cu", "shard.cu", "comm.cu", "ipm_api.cu"]
+SOURCES = ["linalg.cu", "compact.cu", "pcg.cu", "ipmops.cu", "shard.cu", "comm.cu", "ipm_api.cu"]
 
 
 def _stale(out: str, deps) -> bool:

@@ -74,6 +74,7 @@ struct Offsets {
     size_t nvec[40];
     size_t mvec[40];
     size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad, gfull, xloc_all;
+    size_t ch0, cw, cs, cspart, chpart;
     int n_nvec, n_mvec;
     int nchunk;
 };
@@ -83,8 +84,15 @@ constexpr int kMVec = 24;   // m-space vectors
 
 // nloc = rows owned by this rank; every n-space vector gets chunk = ceil(n/P) (+2 pad) slots
 // so the allgather can send equal blocks and the bulk GEMV may read one padding element.
-Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks, Layout &L) {
+Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks, Layout &L, int64_t ldu = 0) {
     Offsets o{};
+    if (ldu > 0) {                     // compact Hessian (NEXT-1): h0, w, s = U^T p and partials
+        o.ch0 = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+        o.cw = L.take(sizeof(double) * ldu);
+        o.cs = L.take(sizeof(double) * ldu);
+        o.cspart = L.take(sizeof(double) * ldu * kCompactGrid);
+        o.chpart = L.take(sizeof(double) * kCompactGrid);
+    }
     const int64_t chunk = (ncols + nranks - 1) / nranks;
     o.sc = L.take(sizeof(Scalars));
     for (int i = 0; i < kNVec; ++i) o.nvec[i] = L.take(sizeof(double) * (std::max<int64_t>(chunk, 1) + 2));
@@ -684,7 +692,9 @@ IPM_EXPORT ipm_status ipm_workspace_size(const ipm_problem *p, const ipm_options
     local_rows(p, row0, nloc);
     if (nloc < 1) return fail(nullptr, IPM_ERR_INVALID, "empty row block");
     Layout L;
-    plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L);   // nnz of the local A^T block <= nnz
+    if (p->hess_kind == 1 && (p->ldu < 1 || p->k < 0 || p->k > p->ldu))
+        return fail(nullptr, IPM_ERR_INVALID, "compact Hessian needs 0 <= k <= ldu and ldu >= 1");
+    plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L, p->hess_kind == 1 ? p->ldu : 0);   // local A^T nnz <= nnz
     *bytes = L.total;
     return IPM_OK;
 }
@@ -761,7 +771,7 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
 
         // --- device state ------------------------------------------------------------
         Layout L;
-        const Offsets o = plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L);
+        const Offsets o = plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L, p->hess_kind == 1 ? p->ldu : 0);
         CK(cudaMemsetAsync(ctx->ws, 0, L.total, ctx->st));
         ctx->sc = reinterpret_cast<Scalars *>(ctx->ws + o.sc);
         assign_vectors(ctx, o);
@@ -815,9 +825,32 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         P.ATcol = ATcol;
         P.ATval = ATval;
         launch_transpose(P, (int)row0, o.nchunk, reinterpret_cast<int *>(ctx->ws + o.cnt), ATrp, ATcol, ATval, ctx->st);
-        launch_setup_diag(P, (int)row0, ctx->st);
         unsigned long long *bad = reinterpret_cast<unsigned long long *>(ctx->ws + o.bad);
-        launch_count_nonfinite(P, bad, ctx->st);
+        if (p->hess_kind == 1) {
+            // compact quasi-Newton Hessian (NEXT-1): h0 and w copied, U borrowed, diag cached
+            P.hess_compact = 1;
+            P.ck = p->k;
+            P.ldu = p->ldu;
+            P.U = p->U;
+            P.h0 = reinterpret_cast<double *>(ctx->ws + o.ch0);
+            P.w = reinterpret_cast<double *>(ctx->ws + o.cw);
+            P.cs = reinterpret_cast<double *>(ctx->ws + o.cs);
+            P.cspart = reinterpret_cast<double *>(ctx->ws + o.cspart);
+            P.chpart = reinterpret_cast<double *>(ctx->ws + o.chpart);
+            CK(cudaMemcpyAsync(P.h0, p->h0, sizeof(double) * nloc, cudaMemcpyDeviceToDevice, ctx->st));
+            if (p->k > 0) CK(cudaMemcpyAsync(P.w, p->w, sizeof(double) * p->k, cudaMemcpyDeviceToDevice, ctx->st));
+            launch_compact_diag(P, ctx->st);
+            if (p->k > 0) {
+                Prob Q = P;                     // non-finite scan over the n x k block of U
+                Q.H = p->U;
+                Q.ldh = p->ldu;
+                Q.ncols = p->k;
+                launch_count_nonfinite(Q, bad, ctx->st);
+            }
+        } else {
+            launch_setup_diag(P, (int)row0, ctx->st);
+            launch_count_nonfinite(P, bad, ctx->st);
+        }
         ctx->launches += 5;
         CKL();
         unsigned long long nbad = 0;
@@ -828,7 +861,7 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         const int gk = ctx->opt.gemv_kernel;
         const bool bulk_ok = gemv_bulk_ok(P);
         bool sym = false;
-        if ((gk == 0 || gk == 3) && !ctx->sharded && bulk_ok) {
+        if ((gk == 0 || gk == 3) && !ctx->sharded && bulk_ok && !P.hess_compact) {
             // the symmetric GEMV reads only H's upper block triangle: require H == H^T bitwise
             unsigned long long nasym = 0;
             CK(cudaMemsetAsync(bad, 0, sizeof nasym, ctx->st));
@@ -847,9 +880,9 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=3 needs an unsharded, exactly symmetric H with even ldh");
         if (gk == 2 && !bulk_ok) return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=2 needs even ldh and 16-byte aligned H");
         P.gemv_sym = sym ? 1 : 0;
-        P.gemv_bulk = (!sym && (gk == 0 || gk == 2) && bulk_ok) ? 1 : 0;
+        P.gemv_bulk = (!sym && !P.hess_compact && (gk == 0 || gk == 2) && bulk_ok) ? 1 : 0;
         P.gemv_bulk_grid = gemv_bulk_grid();
-        ctx->ncb = sym ? sym_ncb((int)p->n) : gemv_ncb((int)p->n);
+        ctx->ncb = P.hess_compact ? 1 : (sym ? sym_ncb((int)p->n) : gemv_ncb((int)p->n));
         P.ncb = ctx->ncb;
         ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
         DBG("create: n=%lld m=%lld nnz=%lld gemv=%s ncb=%d G=%d sharded=%d\n", (long long)p->n, (long long)p->m,
@@ -869,8 +902,11 @@ IPM_EXPORT ipm_status ipm_create(ipm_ctx **out, const ipm_problem *p, const ipm_
     if (p->n > INT32_MAX || p->m > INT32_MAX || p->nnz >= INT32_MAX)
         return fail(nullptr, IPM_ERR_INVALID, "dimension exceeds int32 index range");
     if (check_partition(p) != IPM_OK) return IPM_ERR_INVALID;
-    if (!p->H || !p->g || !p->xl || !p->xu || (p->m > 0 && (!p->l || !p->u || !p->A_rowptr)) ||
-        (p->nnz > 0 && (!p->A_col || !p->A_val)))
+    if (p->hess_kind != 0 && p->hess_kind != 1) return fail(nullptr, IPM_ERR_INVALID, "unknown hess_kind");
+    if (p->hess_kind == 1 && (p->comm_kind != 0 || !p->h0 || !p->U || (p->k > 0 && !p->w)))
+        return fail(nullptr, IPM_ERR_INVALID, "compact Hessian: needs h0, U (and w when k > 0); unsharded only");
+    if ((p->hess_kind == 0 && !p->H) || !p->g || !p->xl || !p->xu ||
+        (p->m > 0 && (!p->l || !p->u || !p->A_rowptr)) || (p->nnz > 0 && (!p->A_col || !p->A_val)))
         return fail(nullptr, IPM_ERR_INVALID, "null data pointer");
     size_t need = 0;
     if (ipm_workspace_size(p, opt, &need) != IPM_OK) return IPM_ERR_INVALID;
@@ -944,7 +980,32 @@ IPM_EXPORT ipm_status ipm_set_linear_term(ipm_ctx *ctx, const double *g) {
 IPM_EXPORT ipm_status ipm_update_hessian_rank2(ipm_ctx *ctx, const double *u, double alpha, const double *v,
                                                double beta) {
     if (!ctx || !u || !v) return fail(ctx, IPM_ERR_INVALID, "null argument");
-    launch_rank2(ctx->P, ctx->row0, u, alpha, v, beta, ctx->st);
+    Prob &P = ctx->P;
+    if (P.hess_compact) {
+        // compact form: append (u, v) as columns k, k+1 with weights (alpha, beta)
+        if (P.ck + 2 > P.ldu)
+            return fail(ctx, IPM_ERR_STATE, "compact Hessian full: k + 2 > ldu (%d + 2 > %lld)", P.ck,
+                        (long long)P.ldu);
+        launch_compact_append(P, P.U, P.ck, u, v, ctx->st);
+        const double wv[2] = {alpha, beta};
+        CK(cudaMemcpyAsync(P.w + P.ck, wv, sizeof wv, cudaMemcpyHostToDevice, ctx->st));
+        P.ck += 2;
+        launch_compact_diag(P, ctx->st);
+        CK(cudaStreamSynchronize(ctx->st));   // wv is a host stack buffer
+        ctx->launches += 2;
+        ctx->graph_ready = false;              // the captured PCG body holds the old k
+        if (ctx->gexec) {
+            cudaGraphExecDestroy(ctx->gexec);
+            ctx->gexec = nullptr;
+        }
+        if (ctx->graph) {
+            cudaGraphDestroy(ctx->graph);
+            ctx->graph = nullptr;
+        }
+        CKL();
+        return IPM_OK;
+    }
+    launch_rank2(P, ctx->row0, u, alpha, v, beta, ctx->st);
     ctx->launches += 1;
     CKL();
     return IPM_OK;

@@ -43,6 +43,13 @@ void launch_transpose(const Prob &P, int col0, int nchunk, int *cnt, int64_t *AT
                       double *ATval, cudaStream_t st);
 void launch_rank2(const Prob &P, int row0, const double *u, double a, const double *v, double b, cudaStream_t st);
 
+// compact.cu (NEXT-1: H = diag(h0) + U diag(w) U^T, matrix-free)
+constexpr int kCompactGrid = 148 * 4;
+void launch_compact_apply(const Prob &P, const double *v, const double *vdot, double *ypart, Scalars *sc, int mode,
+                          int cid, cudaStream_t st);
+void launch_compact_diag(const Prob &P, cudaStream_t st);
+void launch_compact_append(const Prob &P, double *U, int col, const double *u, const double *v, cudaStream_t st);
+
 // pcg.cu
 void launch_pcg_init(const Prob &P, const Vecs &V, Scalars *sc, const double *rhs, double *x, double rtol,
                      double atol, int64_t maxit, int keep_x, cudaStream_t st);

@@ -122,6 +122,10 @@ void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypa
                  double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st) {
     const bool vec = ((P.ldh & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.H) & 15) == 0);
     if (P.n == 0) return;
+    if (P.hess_compact) {                  // NEXT-1: H p = h0 o p + U (w o (U^T p)), ncb = 1
+        launch_compact_apply(P, v, vdot, ypart, sc, mode, cid, st);
+        return;
+    }
     if (P.gemv_sym) {
         launch_symv_bulk(P, v, vdot, ypart, dpart, sc, P.gemv_bulk_grid, mode, cid, st);
         return;

@@ -78,6 +78,13 @@ struct Prob {
     int gemv_sym;          // 1: symmetric upper-triangle TMA-bulk GEMV (k_symv_bulk)
     int ncb;               // column blocks of the ypart[row][cb] layout of the chosen GEMV
     const void *tmap_sym;  // host copy of the CUtensorMap over H (16 x 256 fp64 boxes)
+    // compact quasi-Newton Hessian H = diag(h0) + U diag(w) U^T (compact.cu)
+    int hess_compact;
+    int ck;                // columns of U in use
+    int64_t ldu;           // leading dimension (= column capacity) of U
+    double *U;             // borrowed, n x ldu row-major
+    double *h0, *w;        // workspace copies (w has capacity ldu)
+    double *cs, *cspart, *chpart;   // s = U^T p (ldu), per-CTA column partials, per-CTA h0 p^2 partials
 };
 
 // Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).

@@ -50,10 +50,13 @@ class QP:
 
     def __init__(self, H, g, A_rowptr, A_col, A_val, l, u, xl, xu, *, ldh: Optional[int] = None,
                  device=None, stream: Optional[torch.cuda.Stream] = None, shard: Optional[dict] = None,
-                 **options):
+                 compact: Optional[dict] = None, **options):
         """shard (row-sharded path): dict(rank, nranks, comm_kind, handle) where
         H holds only this rank's row block (see paper_2405_03584_b200.dist.partition) and
-        handle is a ctypes pointer to an ncclUniqueId (comm_kind 1) or an ipm_group (2)."""
+        handle is a ctypes pointer to an ncclUniqueId (comm_kind 1) or an ipm_group (2).
+        compact (matrix-free quasi-Newton H = diag(h0) + U diag(w) U^T, eq:bfgs_hessian, SURVEY
+        NEXT-1): dict(h0=(n,), U=(n, ldu) row-major with the first k columns in use, w=(k,), k);
+        H is then ignored (may be None) and rank-2 updates append columns of U."""
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2405_03584_b200 needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -61,6 +64,11 @@ class QP:
         f64 = torch.float64
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             n = int(g.shape[0])
+            if H is None:
+                if compact is None:
+                    raise ValueError("H is required unless compact= is given")
+                H = torch.zeros(2, dtype=f64, device=self.device)   # placeholder, not read
+                ldh = n
             if isinstance(H, np.ndarray):
                 H = torch.from_numpy(H)
             if H.device.type != "cuda":
@@ -88,6 +96,16 @@ class QP:
             prob.l, prob.u, prob.xl, prob.xu = self.l.data_ptr(), self.u.data_ptr(), self.xl.data_ptr(), self.xu.data_ptr()
             prob.row_begin, prob.row_end, prob.rank, prob.nranks = 0, n, 0, 1
             self.row0, self.nloc = 0, n
+            if compact is not None:
+                self.c_h0 = _dev(compact["h0"], f64, self.device)
+                Uc = compact["U"]
+                if isinstance(Uc, np.ndarray):
+                    Uc = torch.from_numpy(np.ascontiguousarray(Uc))
+                self.c_U = Uc.to(self.device, f64).contiguous()
+                self.c_w = _dev(compact["w"], f64, self.device) if int(compact["k"]) > 0 else torch.zeros(1, dtype=f64,
+                                                                                                     device=self.device)
+                prob.hess_kind, prob.k, prob.ldu = 1, int(compact["k"]), int(self.c_U.shape[1])
+                prob.h0, prob.U, prob.w = self.c_h0.data_ptr(), self.c_U.data_ptr(), self.c_w.data_ptr()
             if shard is not None:
                 from .dist import partition
                 P = int(shard["nranks"])

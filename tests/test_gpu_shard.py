@@ -55,7 +55,7 @@ def test_nccl_transport_single_rank():
     the sharded path and reproduces the unsharded solve bitwise."""
     from paper_2405_03584_b200 import QP
     from paper_2405_03584_b200.dist import nccl_shard, nccl_unique_id
-    q = config("C1", 2)
+    q = planted_qp(600, 150, density=0.03, rank=32, seed=21, rows="mixed", var="mixed")   # n > kSmallN
     t = problem_tensors(q, DEV)
     a = QP(device=DEV, gemv_kernel=2, **t)
     a.solve()
