@@ -33,14 +33,17 @@ k_compact_ut(int n, int k, const double *__restrict__ U, int64_t ldu, const doub
     for (int cs = 0; cs < k; cs += blockDim.x) {
         const int c = cs + threadIdx.x;
         if (c < k) {
-            double acc0 = 0.0, acc1 = 0.0;
+            // eight independent chains (rows i + j, j < 8): enough loads in flight per SM to
+            // stream U at HBM rate; fixed association -> deterministic
+            double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             int64_t i = r0;
-            for (; i + 1 < r1; i += 2) {         // two independent chains
-                acc0 = fma(__ldcs(U + i * ldu + c), __ldg(p + i), acc0);
-                acc1 = fma(__ldcs(U + (i + 1) * ldu + c), __ldg(p + i + 1), acc1);
+            for (; i + 7 < r1; i += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = fma(__ldcs(U + (i + j) * ldu + c), __ldg(p + i + j), acc[j]);
             }
-            if (i < r1) acc0 = fma(__ldcs(U + i * ldu + c), __ldg(p + i), acc0);
-            spart[(int64_t)blockIdx.x * k + c] = acc0 + acc1;
+            for (int j = 0; i < r1; ++i, ++j) acc[j] = fma(__ldcs(U + i * ldu + c), __ldg(p + i), acc[j]);
+            spart[(int64_t)blockIdx.x * k + c] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) +
+                                                 ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         }
     }
     if (pdot_vec) {                              // this CTA's part of sum_i h0_i p_i^2
