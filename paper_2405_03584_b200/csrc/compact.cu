@@ -21,30 +21,41 @@ namespace ipm {
 
 constexpr int kCompactThreads = 256;   // >= k (columns) — checked at create (k <= 256 per pass slice)
 
-__global__ void __launch_bounds__(kCompactThreads)
+constexpr int kUtThreads = 1024;       // 4 row groups x 256 column slots
+constexpr int kUtGroups = kUtThreads / 256;
+
+__global__ void __launch_bounds__(kUtThreads, 1)
 k_compact_ut(int n, int k, const double *__restrict__ U, int64_t ldu, const double *__restrict__ p,
              double *__restrict__ spart, double *__restrict__ hpart, double *__restrict__ s,
              const double *__restrict__ h0, const double *__restrict__ w, const double *__restrict__ pdot_vec,
              Scalars *sc, int cid, int mode) {
-    __shared__ double red[kCompactThreads / 32];
+    __shared__ double red[kUtThreads / 32];
+    __shared__ double grp[kUtGroups][256];
     if (mode == 1 && sc->done) return;
     const int64_t r0 = (int64_t)n * blockIdx.x / gridDim.x, r1 = (int64_t)n * (blockIdx.x + 1) / gridDim.x;
-    // column slices of blockDim columns; thread c sums column cs + c over this CTA's rows, in order
-    for (int cs = 0; cs < k; cs += blockDim.x) {
-        const int c = cs + threadIdx.x;
+    const int slot = threadIdx.x & 255, gq = threadIdx.x >> 8;
+    // column slices of 256: thread (gq, slot) sums column cs + slot over rows r0 + gq + 4 t of
+    // this CTA's range with eight independent chains (~50 KB of U in flight per SM); the four
+    // row groups are then added in group order — a fixed association, deterministic
+    for (int cs = 0; cs < k; cs += 256) {
+        const int c = cs + slot;
+        double part = 0.0;
         if (c < k) {
-            // eight independent chains (rows i + j, j < 8): enough loads in flight per SM to
-            // stream U at HBM rate; fixed association -> deterministic
             double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            int64_t i = r0;
-            for (; i + 7 < r1; i += 8) {
+            int64_t i = r0 + gq;
+            for (; i + 7 * kUtGroups < r1; i += 8 * kUtGroups) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j] = fma(__ldcs(U + (i + j) * ldu + c), __ldg(p + i + j), acc[j]);
+                for (int j = 0; j < 8; ++j)
+                    acc[j] = fma(__ldcs(U + (i + j * kUtGroups) * ldu + c), __ldg(p + i + j * kUtGroups), acc[j]);
             }
-            for (int j = 0; i < r1; ++i, ++j) acc[j] = fma(__ldcs(U + i * ldu + c), __ldg(p + i), acc[j]);
-            spart[(int64_t)blockIdx.x * k + c] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) +
-                                                 ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+            for (int j = 0; i < r1; i += kUtGroups, ++j) acc[j] = fma(__ldcs(U + i * ldu + c), __ldg(p + i), acc[j]);
+            part = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         }
+        grp[gq][slot] = part;
+        __syncthreads();
+        if (gq == 0 && c < k)
+            spart[(int64_t)blockIdx.x * k + c] = (grp[0][slot] + grp[1][slot]) + (grp[2][slot] + grp[3][slot]);
+        __syncthreads();
     }
     if (pdot_vec) {                              // this CTA's part of sum_i h0_i p_i^2
         double hp = 0.0;
@@ -53,11 +64,19 @@ k_compact_ut(int n, int k, const double *__restrict__ U, int64_t ldu, const doub
         if (threadIdx.x == 0) hpart[blockIdx.x] = b;
     }
     if (last_block(&sc->counters[cid])) {
-        // s_c = sum over CTAs in CTA order; p^T H p = sum h0 p^2 + sum_c w_c s_c^2
+        // s_c = sum over CTAs (eight interleaved chains b = j mod 8, then a fixed tree);
+        // p^T H p = sum h0 p^2 + sum_c w_c s_c^2
         double wss = 0.0;
         for (int c = threadIdx.x; c < k; c += blockDim.x) {
-            double t = 0.0;
-            for (int b = 0; b < (int)gridDim.x; ++b) t += ((volatile double *)spart)[(int64_t)b * k + c];
+            double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            const int G = (int)gridDim.x;
+            int b = 0;
+            for (; b + 7 < G; b += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] += __ldcg(spart + (int64_t)(b + j) * k + c);
+            }
+            for (int j = 0; b < G; ++b, ++j) acc[j] += __ldcg(spart + (int64_t)b * k + c);
+            const double t = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
             s[c] = t;
             wss = fma(w[c] * t, t, wss);
         }
@@ -93,7 +112,7 @@ k_compact_us(int n, int k, const double *__restrict__ U, int64_t ldu, const doub
 void launch_compact_apply(const Prob &P, const double *v, const double *vdot, double *ypart, Scalars *sc, int mode,
                           int cid, cudaStream_t st) {
     if (P.n == 0) return;
-    k_compact_ut<<<kCompactGrid, kCompactThreads, 0, st>>>(P.n, P.ck, P.U, P.ldu, v, P.cspart, P.chpart, P.cs, P.h0,
+    k_compact_ut<<<kCompactGrid, kUtThreads, 0, st>>>(P.n, P.ck, P.U, P.ldu, v, P.cspart, P.chpart, P.cs, P.h0,
                                                          P.w, vdot, sc, cid, mode);
     const int g2 = (int)std::min<int64_t>(kMaxGrid, (P.n + 7) / 8);
     k_compact_us<<<g2, kCompactThreads, sizeof(double) * (P.ck > 0 ? P.ck : 1), st>>>(P.n, P.ck, P.U, P.ldu, P.cs, P.w,

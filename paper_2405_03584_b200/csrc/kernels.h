@@ -44,7 +44,7 @@ void launch_transpose(const Prob &P, int col0, int nchunk, int *cnt, int64_t *AT
 void launch_rank2(const Prob &P, int row0, const double *u, double a, const double *v, double b, cudaStream_t st);
 
 // compact.cu (NEXT-1: H = diag(h0) + U diag(w) U^T, matrix-free)
-constexpr int kCompactGrid = 148 * 4;
+constexpr int kCompactGrid = 148;   // U^T p: one 1024-thread CTA per SM
 void launch_compact_apply(const Prob &P, const double *v, const double *vdot, double *ypart, Scalars *sc, int mode,
                           int cid, cudaStream_t st);
 void launch_compact_diag(const Prob &P, cudaStream_t st);
