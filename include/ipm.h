@@ -80,6 +80,10 @@ typedef struct {
                                    tiles, 2 TMA-bulk mbarrier pipeline, 3 symmetric upper-triangle TMA-bulk */
     int32_t pcg_warm_start;     /* 0: each PCG starts from x0 = 0 (default, R11); 1: from the previous
                                    search direction (S:248 option) */
+    int32_t pcg_system;         /* 0: PCG on the condensed system K dx = rhs (D1, default);
+                                   1: PCG on the doubly augmented system eq:2x2_augmented,
+                                   unknowns (dx, dlam_lA, dlam_uA), Jacobi preconditioner on its diagonal;
+                                   unsharded only, and ipm_pcg() is then rejected (IPM_ERR_STATE) */
 } ipm_options;
 
 /* Problem description for ipm_create.  Large arrays are BORROWED (the caller keeps them

@@ -80,7 +80,7 @@ struct Offsets {
 };
 
 constexpr int kNVec = 30;   // n-space vectors in Vecs (see assign_vectors)
-constexpr int kMVec = 24;   // m-space vectors
+constexpr int kMVec = 38;   // m-space vectors (24 + 14 segments of the doubly augmented PCG)
 
 // nloc = rows owned by this rank; every n-space vector gets chunk = ceil(n/P) (+2 pad) slots
 // so the allgather can send equal blocks and the bulk GEMV may read one padding element.
@@ -219,6 +219,9 @@ void assign_vectors(ipm_ctx *c, const Offsets &o) {
     V.ds_lA = mv[j++]; V.ds_uA = mv[j++]; V.dl_lA = mv[j++]; V.dl_uA = mv[j++];
     V.ads_lA = mv[j++]; V.ads_uA = mv[j++]; V.adl_lA = mv[j++]; V.adl_uA = mv[j++];
     V.lamd = mv[j++]; V.pt = mv[j++];
+    V.ag.xl = mv[j++]; V.ag.xu = mv[j++]; V.ag.rl = mv[j++]; V.ag.ru = mv[j++]; V.ag.zl = mv[j++]; V.ag.zu = mv[j++];
+    V.ag.pl = mv[j++]; V.ag.pu = mv[j++]; V.ag.yl = mv[j++]; V.ag.yu = mv[j++]; V.ag.Dl = mv[j++]; V.ag.Du = mv[j++];
+    V.ag.Ml = mv[j++]; V.ag.Mu = mv[j++];
     V.ypart = reinterpret_cast<double *>(b + o.ypart);
     for (int i = 0; i < 8; ++i) V.part[i] = reinterpret_cast<double *>(b + o.part) + (size_t)i * kMaxPartials;
     V.gfull = reinterpret_cast<double *>(b + o.gfull);
@@ -275,10 +278,15 @@ ipm_status op_apply(ipm_ctx *ctx, const double *v_local, const double *v_full, d
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
     if (!v_full) TRY(gather(ctx, v_local, &v_full));
-    launch_spmv(P, v_full, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 0, ctx->st);
+    // mode 1 on an augmented context: the true residual of eq:2x2_augmented, whose dlam
+    // segments are the PCG's own (V.ag.x*); the public operator (mode 0) stays condensed
+    const bool aug = P.aug && mode == 1;
+    const AugArgs ag = aug_args(P, V);
+    if (aug) launch_spmv_aug(P, V, v_full, V.ag.xl, V.ag.xu, ctx->sc, 0, ctx->st);
+    else launch_spmv(P, v_full, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 0, ctx->st);
     launch_gemv(P, v_full, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
     launch_apply_reduce(P, ctx->G, ctx->ncb, V.ypart, V.sig_b, v_local, V.pt, out, rhs, V.part[5], ctx->sc, mode,
-                        ctx->st);
+                        ctx->st, aug ? &ag : nullptr);
     ctx->launches += (P.m > 0 ? 1 : 0) + 2;
     CKL();
     if (mode == 1) TRY(xcombine(ctx, X_RES2));
@@ -351,7 +359,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
         TRY(xcombine(ctx, X_PCG_RESTART));
     }
     ctx->have_dx = true;
-    const bool small = !ctx->sharded && P.n <= kSmallN && ctx->opt.use_graph;
+    const bool small = !ctx->sharded && !P.aug && P.n <= kSmallN && ctx->opt.use_graph;
     const bool graph = ctx->opt.use_graph && !ctx->sharded && !small;
     if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
@@ -884,6 +892,10 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         P.gemv_bulk_grid = gemv_bulk_grid();
         ctx->ncb = P.hess_compact ? 1 : (sym ? sym_ncb((int)p->n) : gemv_ncb((int)p->n));
         P.ncb = ctx->ncb;
+        if (ctx->opt.pcg_system != 0 && ctx->opt.pcg_system != 1) return fail(ctx, IPM_ERR_INVALID, "unknown pcg_system");
+        if (ctx->opt.pcg_system == 1 && ctx->sharded)
+            return fail(ctx, IPM_ERR_INVALID, "pcg_system = 1 (doubly augmented) is unsharded only");
+        P.aug = (ctx->opt.pcg_system == 1 && p->m > 0) ? 1 : 0;
         ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
         DBG("create: n=%lld m=%lld nnz=%lld gemv=%s ncb=%d G=%d sharded=%d\n", (long long)p->n, (long long)p->m,
             (long long)p->nnz, sym ? "symmetric-bulk" : (P.gemv_bulk ? "bulk" : "ldg"), ctx->ncb, ctx->G,
@@ -1092,6 +1104,7 @@ IPM_EXPORT ipm_status ipm_op_diag(ipm_ctx *ctx, const double *sig_b, const doubl
 IPM_EXPORT ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *rhs, double *x,
                               double rtol, int32_t *iters) {
     if (!ctx || !sig_b || !rhs || !x || (ctx->m > 0 && !sig_c)) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    if (ctx->P.aug) return fail(ctx, IPM_ERR_STATE, "ipm_pcg solves the condensed system: create with pcg_system = 0");
     TRY(load_sigmas(ctx, sig_b, sig_c));
     launch_jacobi(ctx->P, ctx->G, ctx->V.sig_b, ctx->V.sig_c, ctx->V.Minv, 1, ctx->st);
     CK(cudaMemcpyAsync(ctx->V.rhs, rhs, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
@@ -1114,6 +1127,7 @@ IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, doub
     auto one = [&]() {
         // what 0: the PCG GEMV's full work (tiles + fused p^T H p) without its done/alpha epilogue
         if (what == 0) launch_gemv(P, V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV_PCG, ctx->st);
+        else if (what == 1 && P.aug) launch_spmv_aug(P, V, V.pp, V.ag.pl, V.ag.pu, ctx->sc, 1, ctx->st);
         else if (what == 1) launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
         else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork);
     };

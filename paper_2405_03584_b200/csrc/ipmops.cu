@@ -321,12 +321,21 @@ void launch_residuals(const Prob &P, const Vecs &V, int G, Scalars *sc, double m
 __global__ void k_sigma_m(int m, const double *__restrict__ l, const double *__restrict__ u,
                           const double *__restrict__ s_l, const double *__restrict__ s_u,
                           const double *__restrict__ lam_l, const double *__restrict__ lam_u,
-                          double *__restrict__ sigc) {
+                          double *__restrict__ sigc, int aug, double *__restrict__ Dl, double *__restrict__ Du,
+                          double *__restrict__ Ml, double *__restrict__ Mu) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         double s = 0.0;
-        if (has(l[i])) s += lam_l[i] / s_l[i];
-        if (has(u[i])) s += lam_u[i] / s_u[i];
+        const bool hl = has(l[i]), hu = has(u[i]);
+        if (hl) s += lam_l[i] / s_l[i];
+        if (hu) s += lam_u[i] / s_u[i];
         sigc[i] = s;
+        if (aug) {   // eq:2x2_augmented: D = S Lam^-1 on the middle rows, Jacobi 1/D (0 on absent rows,
+                     // which keeps their z, p and dlam at exactly 0)
+            Dl[i] = hl ? s_l[i] / lam_l[i] : 0.0;
+            Du[i] = hu ? s_u[i] / lam_u[i] : 0.0;
+            Ml[i] = hl ? lam_l[i] / s_l[i] : 0.0;
+            Mu[i] = hu ? lam_u[i] / s_u[i] : 0.0;
+        }
     }
 }
 
@@ -336,7 +345,7 @@ k_sigma_n_jacobi(int n, const double *__restrict__ xl, const double *__restrict_
                  const double *__restrict__ s_u, const double *__restrict__ lam_l, const double *__restrict__ lam_u,
                  const double *__restrict__ diagH, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol,
                  const double *__restrict__ ATval, const double *__restrict__ sigc, double *__restrict__ sigb,
-                 double *__restrict__ Minv) {
+                 double *__restrict__ Minv, double cfac) {
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
     // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
@@ -357,19 +366,20 @@ k_sigma_n_jacobi(int n, const double *__restrict__ xl, const double *__restrict_
             if (has(xl[j])) sb += lam_l[j] / s_l[j];
             if (has(xu[j])) sb += lam_u[j] / s_u[j];
             sigb[j] = sb;
-            Minv[j] = 1.0 / (diagH[j] + sb + s);
+            Minv[j] = 1.0 / (diagH[j] + sb + cfac * s);   // cfac = 2 on the augmented top block
         }
     }
 }
 
 void launch_sigma(const Prob &P, const Vecs &V, int G, cudaStream_t st) {
     if (P.m > 0)
-        k_sigma_m<<<grid_for(P.m, kBlock), kBlock, 0, st>>>(P.m, P.l, P.u, V.s_lA, V.s_uA, V.lam_lA, V.lam_uA, V.sig_c);
+        k_sigma_m<<<grid_for(P.m, kBlock), kBlock, 0, st>>>(P.m, P.l, P.u, V.s_lA, V.s_uA, V.lam_lA, V.lam_uA, V.sig_c,
+                                                           P.aug, V.ag.Dl, V.ag.Du, V.ag.Ml, V.ag.Mu);
     const double *sigc = (P.m > 0) ? V.sig_c : nullptr;
     const int grid = grid_for(P.n, kBlock / G);
     IPM_DISPATCH_G(G, (k_sigma_n_jacobi<GG><<<grid, kBlock, 0, st>>>(P.n, P.xl, P.xu, V.s_lx, V.s_ux, V.lam_lx, V.lam_ux,
                                                                      P.diagH, P.ATrp, P.ATcol, P.ATval, sigc, V.sig_b,
-                                                                     V.Minv)));
+                                                                     V.Minv, P.aug ? 2.0 : 1.0)));
 }
 
 // ------------------------------------------------------------------------------ RHS
@@ -418,7 +428,7 @@ k_rhs_n(int n, const double *__restrict__ xl, const double *__restrict__ xu, con
         const double *__restrict__ adl_l, const double *__restrict__ ads_l, const double *__restrict__ adl_u,
         const double *__restrict__ ads_u, double *__restrict__ rc_l, double *__restrict__ rc_u,
         const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, const double *__restrict__ ATval,
-        const double *__restrict__ w, double *__restrict__ rhs, double mu, int mode, double smu) {
+        const double *__restrict__ w, double *__restrict__ rhs, double mu, int mode, double smu, double wfac) {
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
     // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
@@ -446,7 +456,7 @@ k_rhs_n(int n, const double *__restrict__ xl, const double *__restrict__ xu, con
             }
             rc_l[j] = ca;
             rc_u[j] = cb;
-            rhs[j] = r1 + at;
+            rhs[j] = fma(wfac, at, r1);   // wfac = 2: top block r1 + 2 B^T D^-1 r2 of eq:2x2_augmented
         }
     }
 }
@@ -461,7 +471,7 @@ void launch_rhs(const Prob &P, const Vecs &V, int G, double mu, int mode, double
     IPM_DISPATCH_G(G, (k_rhs_n<GG><<<grid, kBlock, 0, st>>>(P.n, P.xl, P.xu, V.s_lx, V.s_ux, V.lam_lx, V.lam_ux, V.r_lx,
                                                             V.r_ux, V.rH, V.adl_lx, V.ads_lx, V.adl_ux, V.ads_ux,
                                                             V.rc_lx, V.rc_ux, P.ATrp, P.ATcol, P.ATval, w, V.rhs, mu,
-                                                            mode, sigma_mu)));
+                                                            mode, sigma_mu, P.aug ? 2.0 : 1.0)));
 }
 
 // ------------------------------------------------------------- recovery + step lengths
@@ -475,7 +485,8 @@ k_recover_m(int m, const double *__restrict__ l, const double *__restrict__ u, c
             const double *__restrict__ r2_u, const double *__restrict__ s_l, const double *__restrict__ s_u,
             const double *__restrict__ lam_l, const double *__restrict__ lam_u, double *__restrict__ ds_l,
             double *__restrict__ ds_u, double *__restrict__ dl_l, double *__restrict__ dl_u,
-            double *__restrict__ p1, double *__restrict__ p2, Scalars *sc) {
+            double *__restrict__ p1, double *__restrict__ p2, Scalars *sc, const double *__restrict__ aug_dl,
+            const double *__restrict__ aug_du) {
     __shared__ double red[kBlock / 32];
     double mx = INFINITY, ml = INFINITY;
     int bad = 0;
@@ -484,14 +495,14 @@ k_recover_m(int m, const double *__restrict__ l, const double *__restrict__ u, c
         double dsl = 0.0, dll = 0.0, dsu = 0.0, dlu = 0.0;
         if (has(l[i])) {
             dsl = a + r_l[i];
-            dll = (r2_l[i] - a) / (s_l[i] / lam_l[i]);
+            dll = aug_dl ? aug_dl[i] : (r2_l[i] - a) / (s_l[i] / lam_l[i]);   // augmented: PCG's dlam
             ratio_min(s_l[i], dsl, mx);
             ratio_min(lam_l[i], dll, ml);
             bad |= !finite_d(dsl) | !finite_d(dll);
         }
         if (has(u[i])) {
             dsu = -a + r_u[i];
-            dlu = (r2_u[i] + a) / (s_u[i] / lam_u[i]);
+            dlu = aug_du ? aug_du[i] : (r2_u[i] + a) / (s_u[i] / lam_u[i]);
             ratio_min(s_u[i], dsu, mx);
             ratio_min(lam_u[i], dlu, ml);
             bad |= !finite_d(dsu) | !finite_d(dlu);
@@ -586,7 +597,8 @@ void launch_recover(const Prob &P, const Vecs &V, Scalars *sc, double tau, int a
     if (P.m > 0)
         k_recover_m<<<grid_for(P.m, kBlock), kBlock, 0, st>>>(P.m, P.l, P.u, V.Adx, V.r_lA, V.r_uA, V.r2_l, V.r2_u,
                                                              V.s_lA, V.s_uA, V.lam_lA, V.lam_uA, dsA_l, dsA_u, dlA_l,
-                                                             dlA_u, V.part[0], V.part[1], sc);
+                                                             dlA_u, V.part[0], V.part[1], sc, P.aug ? V.ag.xl : nullptr,
+                                                             P.aug ? V.ag.xu : nullptr);
     k_recover_n<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, P.xl, P.xu, V.dx, V.r_lx, V.r_ux, V.rc_lx, V.rc_ux,
                                                          V.s_lx, V.s_ux, V.lam_lx, V.lam_ux, dsx_l, dsx_u, dlx_l, dlx_u,
                                                          V.part[2], V.part[3], sc, tau);

@@ -32,9 +32,14 @@ void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double
                       Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
                  Scalars *sc, int mode, int check_done, cudaStream_t st);
+// NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,
+// yu = -A px + D_u pu (masked); mode 1 (PCG): done check + S_c = a.t + pl.yl + pu.yu
+void launch_spmv_aug(const Prob &P, const Vecs &V, const double *px, const double *pl, const double *pu, Scalars *sc,
+                     int mode, cudaStream_t st);
+AugArgs aug_args(const Prob &P, const Vecs &V);
 void launch_apply_reduce(const Prob &P, int G, int ncb, const double *ypart, const double *sigb,
                          const double *v, const double *t, double *y, const double *rhs, double *dpart,
-                         Scalars *sc, int mode, cudaStream_t st);
+                         Scalars *sc, int mode, cudaStream_t st, const AugArgs *ag = nullptr);
 void launch_jacobi(const Prob &P, int G, const double *sigb, const double *sigc, double *out, int invert,
                    cudaStream_t st);
 void launch_setup_diag(const Prob &P, int row0, cudaStream_t st);

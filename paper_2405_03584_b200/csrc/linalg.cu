@@ -647,6 +647,70 @@ void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, 
         k_spmv<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV, check_done);
 }
 
+// ------------------------------------------------ doubly augmented operator, SpMV stage (NEXT-2)
+// eq:2x2_augmented with B = [A_l; -A_u], D = S Lam^-1:
+//   top   = Q v_x + 2 B^T D^-1 B v_x + B^T v_lam = H v_x + Sigma_b v_x + A^T (2 Sigma_c a + v_l - v_u)
+//   mid_l =  a + D_l v_l ,   mid_u = -a + D_u v_u ,   a = A v_x     (rows of absent bounds are 0)
+// This kernel produces t = 2 Sigma_c a + v_l - v_u (gathered later by the A^T-row groups), the
+// middle rows, and (MODE 1) their share of p^T K p: a.t + p_l.mid_l + p_u.mid_u.
+__device__ __forceinline__ bool has_b(double b) { return fabs(b) < INFINITY; }
+
+template <int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_spmv_aug(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const double *__restrict__ val,
+           const double *__restrict__ px, const double *__restrict__ pl, const double *__restrict__ pu,
+           const double *__restrict__ l, const double *__restrict__ u, const double *__restrict__ sigc,
+           const double *__restrict__ Dl, const double *__restrict__ Du, double *__restrict__ t,
+           double *__restrict__ yl, double *__restrict__ yu, double *__restrict__ dpart, Scalars *sc, int cid) {
+    __shared__ double red[kBlock / 32];
+    if (MODE == 1 && sc->done) return;
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    double dacc = 0.0;
+    for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
+        const int64_t s0 = rp[i], e = rp[i + 1];
+        double a = 0.0;
+        for (int64_t k = s0 + lane; k < e; k += 32) a = fma(__ldg(val + k), __ldg(px + __ldg(col + k)), a);
+        a = warp_sum(a);
+        if (lane == 0) {
+            const double vl = pl[i], vu = pu[i];
+            const double ml = has_b(l[i]) ? fma(Dl[i], vl, a) : 0.0;
+            const double mu = has_b(u[i]) ? fma(Du[i], vu, -a) : 0.0;
+            const double ti = fma(2.0 * sigc[i], a, vl - vu);
+            t[i] = ti;
+            yl[i] = ml;
+            yu[i] = mu;
+            if (MODE == 1) {
+                dacc = fma(a, ti, dacc);
+                dacc = fma(vl, ml, dacc);
+                dacc = fma(vu, mu, dacc);
+            }
+        }
+    }
+    if (MODE == 0) return;
+    const double bs = block_sum(dacc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
+    if (last_block(&sc->counters[cid])) {
+        const double tot = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[cid] = 0;
+            sc->S_c = tot;
+        }
+    }
+}
+
+void launch_spmv_aug(const Prob &P, const Vecs &V, const double *px, const double *pl, const double *pu, Scalars *sc,
+                     int mode, cudaStream_t st) {
+    if (P.m == 0) return;
+    const int grid = grid_for(P.m, kBlock / 32);
+    if (mode == 1)
+        k_spmv_aug<1><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, px, pl, pu, P.l, P.u, V.sig_c, V.ag.Dl,
+                                               V.ag.Du, V.pt, V.ag.yl, V.ag.yu, V.part[3], sc, C_SPMV_PCG);
+    else
+        k_spmv_aug<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, px, pl, pu, P.l, P.u, V.sig_c, V.ag.Dl,
+                                               V.ag.Du, V.pt, V.ag.yl, V.ag.yu, V.part[3], sc, C_SPMV);
+}
+
 // ------------------------------------------------------ y = sum_cb ypart + sig_b v + A^T t
 // MODE 0: write y.  MODE 1: r = rhs - y, res2 = ||r||^2 (true residual of PCG).
 // MODE 2: y = sum_cb ypart only (plain H v, for residuals), also obj/dots not needed.
@@ -655,7 +719,7 @@ __global__ void __launch_bounds__(kBlock)
 k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
                const double *__restrict__ v, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol,
                const double *__restrict__ ATval, const double *__restrict__ t, double *__restrict__ y,
-               const double *__restrict__ rhs, double *__restrict__ dpart, Scalars *sc, int cid) {
+               const double *__restrict__ rhs, double *__restrict__ dpart, Scalars *sc, int cid, AugArgs ag) {
     __shared__ double red[kBlock / 32];
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
@@ -683,6 +747,15 @@ k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *_
         }
     }
     if (MODE != 1) return;
+    if (ag.on) {                    // doubly augmented: r_l = rhs_l - y_l, r_u = rhs_u - y_u
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ag.m; i += gridDim.x * blockDim.x) {
+            const double a = ag.rhsl[i] - ag.yl[i], b = ag.rhsu[i] - ag.yu[i];
+            ag.rl[i] = a;
+            ag.ru[i] = b;
+            acc = fma(a, a, acc);
+            acc = fma(b, b, acc);
+        }
+    }
     const double bs = block_sum(acc, red);
     if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
     if (last_block(&sc->counters[cid])) {
@@ -705,16 +778,18 @@ k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *_
 
 void launch_apply_reduce(const Prob &P, int G, int ncb, const double *ypart, const double *sigb,
                          const double *v, const double *t, double *y, const double *rhs, double *dpart,
-                         Scalars *sc, int mode, cudaStream_t st) {
+                         Scalars *sc, int mode, cudaStream_t st, const AugArgs *agp) {
     if (P.n == 0) return;
     const int grid = grid_for(P.n, kBlock / G);
     const double *tt = (P.m > 0) ? t : nullptr;
+    AugArgs ag{};
+    if (agp && mode == 1) ag = *agp;
     if (mode == 0) {
-        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 0><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES)));
+        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 0><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES, ag)));
     } else if (mode == 1) {
-        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 1><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES)));
+        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 1><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES, ag)));
     } else {
-        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 2><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES)));
+        IPM_DISPATCH_G(G, (k_apply_reduce<GG, 2><<<grid, kBlock, 0, st>>>(P.n, ncb, ypart, sigb, v, P.ATrp, P.ATcol, P.ATval, tt, y, rhs, dpart, sc, C_TRUE_RES, ag)));
     }
 }
 

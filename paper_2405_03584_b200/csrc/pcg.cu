@@ -16,6 +16,7 @@
 #include "state.h"
 #include "finalize.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -45,7 +46,7 @@ static int grid_for(int64_t units, int per_block) {
 __global__ void __launch_bounds__(kBlock)
 k_pcg_init(int n, const double *__restrict__ rhs, double *__restrict__ x, double *__restrict__ r,
            double *__restrict__ z, const double *__restrict__ Minv, double *__restrict__ p1,
-           double *__restrict__ p2, int keep_x, Scalars *sc, double rtol, double atol, int64_t maxit) {
+           double *__restrict__ p2, int keep_x, Scalars *sc, double rtol, double atol, int64_t maxit, AugArgs ag) {
     __shared__ double red[kBlock / 32];
     double rz = 0.0, rr = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -56,6 +57,24 @@ k_pcg_init(int n, const double *__restrict__ rhs, double *__restrict__ x, double
         z[i] = zi;
         rz = fma(ri, zi, rz);
         rr = fma(ri, ri, rr);
+    }
+    if (ag.on) {                        // doubly augmented system: the dlam_l / dlam_u segments
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ag.m; i += gridDim.x * blockDim.x) {
+            const double a = ag.rhsl[i], b = ag.rhsu[i];
+            const double za = ag.Ml[i] * a, zb = ag.Mu[i] * b;
+            if (!keep_x) {
+                ag.xl[i] = 0.0;
+                ag.xu[i] = 0.0;
+            }
+            ag.rl[i] = a;
+            ag.ru[i] = b;
+            ag.zl[i] = za;
+            ag.zu[i] = zb;
+            rz = fma(a, za, rz);
+            rz = fma(b, zb, rz);
+            rr = fma(a, a, rr);
+            rr = fma(b, b, rr);
+        }
     }
     const double a = block_sum(rz, red);
     const double b = block_sum(rr, red);
@@ -78,17 +97,38 @@ k_pcg_init(int n, const double *__restrict__ rhs, double *__restrict__ x, double
     }
 }
 
+AugArgs aug_args(const Prob &P, const Vecs &V) {
+    AugArgs a{};
+    a.on = P.aug;
+    a.m = P.m;
+    a.xl = V.ag.xl;
+    a.xu = V.ag.xu;
+    a.rl = V.ag.rl;
+    a.ru = V.ag.ru;
+    a.zl = V.ag.zl;
+    a.zu = V.ag.zu;
+    a.pl = V.ag.pl;
+    a.pu = V.ag.pu;
+    a.yl = V.ag.yl;
+    a.yu = V.ag.yu;
+    a.Ml = V.ag.Ml;
+    a.Mu = V.ag.Mu;
+    a.rhsl = V.r2_l;
+    a.rhsu = V.r2_u;
+    return a;
+}
+
 void launch_pcg_init(const Prob &P, const Vecs &V, Scalars *sc, const double *rhs, double *x, double rtol,
                      double atol, int64_t maxit, int keep_x, cudaStream_t st) {
-    const int grid = grid_for(P.n, kBlock);
+    const int grid = grid_for(std::max(P.n, P.aug ? P.m : 0), kBlock);
     k_pcg_init<<<grid, kBlock, 0, st>>>(P.n, rhs, x, V.pr, V.pz, V.Minv, V.part[0], V.part[1], keep_x, sc, rtol,
-                                        atol, maxit);
+                                        atol, maxit, aug_args(P, V));
 }
 
 // After the true-residual check (r already holds rhs - K x): z = M^-1 r, rho = r^T z, restart.
 __global__ void __launch_bounds__(kBlock)
 k_pcg_restart(int n, const double *__restrict__ r, double *__restrict__ z, const double *__restrict__ Minv,
-              double *__restrict__ p1, double *__restrict__ p2, Scalars *sc) {
+              double *__restrict__ p1, double *__restrict__ p2, Scalars *sc, AugArgs ag) {
     __shared__ double red[kBlock / 32];
     double rz = 0.0, rr = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -97,6 +137,18 @@ k_pcg_restart(int n, const double *__restrict__ r, double *__restrict__ z, const
         z[i] = zi;
         rz = fma(ri, zi, rz);
         rr = fma(ri, ri, rr);
+    }
+    if (ag.on) {
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ag.m; i += gridDim.x * blockDim.x) {
+            const double a = ag.rl[i], b = ag.ru[i];
+            const double za = ag.Ml[i] * a, zb = ag.Mu[i] * b;
+            ag.zl[i] = za;
+            ag.zu[i] = zb;
+            rz = fma(a, za, rz);
+            rz = fma(b, zb, rz);
+            rr = fma(a, a, rr);
+            rr = fma(b, b, rr);
+        }
     }
     const double a = block_sum(rz, red);
     const double b = block_sum(rr, red);
@@ -120,7 +172,8 @@ k_pcg_restart(int n, const double *__restrict__ r, double *__restrict__ z, const
 }
 
 void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
-    k_pcg_restart<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, V.pr, V.pz, V.Minv, V.part[0], V.part[1], sc);
+    k_pcg_restart<<<grid_for(std::max(P.n, P.aug ? P.m : 0), kBlock), kBlock, 0, st>>>(
+        P.n, V.pr, V.pz, V.Minv, V.part[0], V.part[1], sc, aug_args(P, V));
 }
 
 __global__ void __launch_bounds__(kBlock)
@@ -145,7 +198,7 @@ void launch_dot2(int n, const double *a, double *dpart, Scalars *sc, cudaStream_
 
 __global__ void __launch_bounds__(kBlock)
 k_pcg_p(int n, const double *__restrict__ z, double *__restrict__ p, const double *__restrict__ sigb,
-        double *__restrict__ dpart, Scalars *sc) {
+        double *__restrict__ dpart, Scalars *sc, AugArgs ag) {
     __shared__ double red[kBlock / 32];
     if (sc->done) return;
     const bool first = (sc->it_rs == 0);
@@ -155,6 +208,12 @@ k_pcg_p(int n, const double *__restrict__ z, double *__restrict__ p, const doubl
         const double pi = first ? z[i] : fma(beta, p[i], z[i]);
         p[i] = pi;
         acc = fma(sigb[i] * pi, pi, acc);
+    }
+    if (ag.on) {                      // p_l, p_u (their p^T K p share comes from k_spmv_aug)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ag.m; i += gridDim.x * blockDim.x) {
+            ag.pl[i] = first ? ag.zl[i] : fma(beta, ag.pl[i], ag.zl[i]);
+            ag.pu[i] = first ? ag.zu[i] : fma(beta, ag.pu[i], ag.zu[i]);
+        }
     }
     const double b = block_sum(acc, red);
     if (threadIdx.x == 0) dpart[blockIdx.x] = b;
@@ -175,7 +234,7 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
              const double *__restrict__ ATval, const double *__restrict__ t, double *__restrict__ x,
              double *__restrict__ r, double *__restrict__ z, const double *__restrict__ Minv,
              double *__restrict__ p1, double *__restrict__ p2, Scalars *sc, cudaGraphConditionalHandle h,
-             int use_cond) {
+             int use_cond, AugArgs ag) {
     __shared__ double red[kBlock / 32];
     if (sc->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
@@ -234,6 +293,22 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
             z[i] = zi;
             rz = fma(ri, zi, rz);
             rr = fma(ri, ri, rr);
+        }
+    }
+    if (ag.on) {                      // dlam_l / dlam_u segments of the doubly augmented system
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ag.m; i += gridDim.x * blockDim.x) {
+            ag.xl[i] = fma(alpha, ag.pl[i], ag.xl[i]);
+            ag.xu[i] = fma(alpha, ag.pu[i], ag.xu[i]);
+            const double ra = fma(-alpha, ag.yl[i], ag.rl[i]), rb = fma(-alpha, ag.yu[i], ag.ru[i]);
+            ag.rl[i] = ra;
+            ag.ru[i] = rb;
+            const double za = ag.Ml[i] * ra, zb = ag.Mu[i] * rb;
+            ag.zl[i] = za;
+            ag.zu[i] = zb;
+            rz = fma(ra, za, rz);
+            rz = fma(rb, zb, rz);
+            rr = fma(ra, ra, rr);
+            rr = fma(rb, rb, rr);
         }
     }
     const double a = block_sum(rz, red);
@@ -350,15 +425,18 @@ void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cuda
 }
 
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
-    k_pcg_p<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2], sc);
+    k_pcg_p<<<grid_for(std::max(P.n, P.aug ? P.m : 0), kBlock), kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2],
+                                                                                sc, aug_args(P, V));
 }
 
-void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st) {
+static void launch_update_g(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x,
+                            cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
     const int ug = grid_for(P.n, kBlock / G);
     const double *t = (P.m > 0) ? V.pt : nullptr;
+    const AugArgs ag = aug_args(P, V);
 #define IPM_UPD(GG)                                                                                              \
     k_pcg_update<GG><<<ug, kBlock, 0, st>>>(P.n, ncb, V.ypart, V.sig_b, V.pp, P.ATrp, P.ATcol, P.ATval, t, x, V.pr, \
-                                            V.pz, V.Minv, V.part[5], V.part[6], sc, 0, 0)
+                                            V.pz, V.Minv, V.part[5], V.part[6], sc, h, use_cond, ag)
     switch (G) {
         case 4: IPM_UPD(4); break;
         case 8: IPM_UPD(8); break;
@@ -368,38 +446,37 @@ void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc
 #undef IPM_UPD
 }
 
+void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st) {
+    launch_update_g(P, V, G, ncb, sc, x, 0, 0, st);
+}
+
+// the SpMV stage of an iteration: condensed t = sig_c o (A p), or (NEXT-2) the augmented
+// t = 2 sig_c o (A p_x) + p_l - p_u and the middle block rows y_l, y_u
+static void spmv_stage(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
+    if (P.aug) launch_spmv_aug(P, V, V.pp, V.ag.pl, V.ag.pu, sc, 1, st);
+    else launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
+}
+
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
                           cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork) {
-    const int grid = grid_for(P.n, kBlock);
-    k_pcg_p<<<grid, kBlock, 0, st>>>(P.n, V.pz, V.pp, V.sig_b, V.part[2], sc);
+    launch_pcg_p(P, V, sc, st);
     if (!use_cond) dstage("pcg_p", st);
-    // t = Sigma_c o (A p) only shares p with the GEMV: run it on a side stream (a parallel
-    // branch of the captured graph) next to the HBM-bound GEMV; joined before the update.
+    // the SpMV stage only shares p with the GEMV: run it on a side stream (a parallel branch of
+    // the captured graph) next to the HBM-bound GEMV; joined before the update.
     const bool par = fork != nullptr && P.m > 0;
     if (par) {
         cudaEventRecord(fork->ev_fork, st);
         cudaStreamWaitEvent(fork->side, fork->ev_fork, 0);
-        launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, fork->side);
+        spmv_stage(P, V, sc, fork->side);
         cudaEventRecord(fork->ev_join, fork->side);
     } else {
-        launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
+        spmv_stage(P, V, sc, st);
         if (!use_cond) dstage("spmv", st);
     }
     launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);
     if (!use_cond) dstage("gemv", st);
     if (par) cudaStreamWaitEvent(st, fork->ev_join, 0);
-    const int ug = grid_for(P.n, kBlock / G);
-    const double *t = (P.m > 0) ? V.pt : nullptr;
-#define IPM_UPD(GG)                                                                                              \
-    k_pcg_update<GG><<<ug, kBlock, 0, st>>>(P.n, ncb, V.ypart, V.sig_b, V.pp, P.ATrp, P.ATcol, P.ATval, t, x, V.pr, \
-                                            V.pz, V.Minv, V.part[5], V.part[6], sc, h, use_cond)
-    switch (G) {
-        case 4: IPM_UPD(4); break;
-        case 8: IPM_UPD(8); break;
-        case 16: IPM_UPD(16); break;
-        default: IPM_UPD(32); break;
-    }
-#undef IPM_UPD
+    launch_update_g(P, V, G, ncb, sc, x, h, use_cond, st);
 }
 
 }  // namespace ipm

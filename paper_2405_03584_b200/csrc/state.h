@@ -85,6 +85,7 @@ struct Prob {
     double *U;             // borrowed, n x ldu row-major
     double *h0, *w;        // workspace copies (w has capacity ldu)
     double *cs, *cspart, *chpart;   // s = U^T p (ldu), per-CTA column partials, per-CTA h0 p^2 partials
+    int aug;               // 1: PCG on the doubly augmented system eq:2x2_augmented
 };
 
 // Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).
@@ -108,6 +109,18 @@ struct Vecs {
     double *gfull;                                   // sharded: gathered full-length vector (P*chunk)
     double *xloc_all;                                // sharded: allgathered loc[] of all ranks (8*P)
     double *part[8];                                 // reduction partials, kMaxPartials each
+    struct {                                         // doubly augmented PCG (NEXT-2), m-space segments
+        double *xl, *xu, *rl, *ru, *zl, *zu, *pl, *pu, *yl, *yu, *Dl, *Du, *Ml, *Mu;
+    } ag;
+};
+
+// Kernel-side view of the augmented segments (on = 0: condensed system, everything ignored).
+struct AugArgs {
+    int on;
+    int m;
+    double *xl, *xu, *rl, *ru, *zl, *zu, *pl, *pu, *yl, *yu;
+    const double *Ml, *Mu;
+    const double *rhsl, *rhsu;   // = r2_l, r2_u (the bottom block of the eq:2x2_augmented rhs)
 };
 
 }  // namespace ipm
