@@ -63,6 +63,31 @@ class ipm_info(C.Structure):
                 ("row_begin", C.c_int64), ("row_end", C.c_int64)]
 
 
+# include/sqp.h
+class ipm_dose_nlp(C.Structure):
+    _fields_ = [("nd", C.c_int64), ("nnz", C.c_int64), ("D_rowptr", C.c_void_p), ("D_col", C.c_void_p),
+                ("D_val", C.c_void_p), ("w", C.c_void_p), ("p", C.c_void_p), ("dmax", C.c_void_p),
+                ("kappa", C.c_void_p), ("beta", C.c_double)]
+
+
+class ipm_sqp_options(C.Structure):
+    _fields_ = [("size", C.c_int32), ("max_iter", C.c_int32), ("tol_d", C.c_double), ("armijo_c1", C.c_double),
+                ("max_backtrack", C.c_int32), ("powell", C.c_double), ("warm_start", C.c_int32),
+                ("hess_kind", C.c_int32), ("max_cols", C.c_int32), ("h0_floor", C.c_double)]
+
+
+class ipm_sqp_stats(C.Structure):
+    _fields_ = [("status", C.c_int32), ("iters", C.c_int32), ("f", C.c_double), ("d_inf", C.c_double),
+                ("ipm_iters_total", C.c_int64), ("pcg_iters_total", C.c_int64), ("updates_skipped", C.c_int32),
+                ("backtracks", C.c_int32), ("t_total_ms", C.c_double), ("t_qp_ms", C.c_double)]
+
+
+class ipm_sqp_trace_rec(C.Structure):
+    _fields_ = [("it", C.c_int32), ("ipm_iters", C.c_int32), ("pcg_iters", C.c_int64), ("f", C.c_double),
+                ("d_inf", C.c_double), ("step", C.c_double), ("theta", C.c_double), ("qp_ms", C.c_double),
+                ("updated", C.c_int32), ("ncols", C.c_int32)]
+
+
 _P = C.c_void_p
 _D = C.c_double
 _S = C.c_int32
@@ -91,6 +116,20 @@ _sigs = {
     "ipm_kernel_launches": ([_P], C.c_int64),
     "ipm_last_error": ([_P], C.c_char_p),
     "ipm_destroy": ([_P], None),
+    "ipm_sqp_options_default": ([C.POINTER(ipm_sqp_options)], None),
+    "ipm_sqp_workspace_size": ([C.POINTER(ipm_problem), C.POINTER(ipm_dose_nlp), C.POINTER(ipm_sqp_options),
+                                C.POINTER(ipm_options), C.POINTER(C.c_size_t)], _S),
+    "ipm_sqp_create": ([C.POINTER(_P), C.POINTER(ipm_problem), C.POINTER(ipm_dose_nlp), C.POINTER(ipm_sqp_options),
+                        C.POINTER(ipm_options), _P, C.c_size_t, _P], _S),
+    "ipm_sqp_solve": ([_P, _P], _S),
+    "ipm_sqp_get_x": ([_P, _P], _S),
+    "ipm_sqp_get_stats": ([_P, C.POINTER(ipm_sqp_stats)], _S),
+    "ipm_sqp_get_trace": ([_P, C.POINTER(ipm_sqp_trace_rec), C.c_int32, C.POINTER(C.c_int32)], _S),
+    "ipm_sqp_eval": ([_P, _P, C.POINTER(_D), _P], _S),
+    "ipm_sqp_qp": ([_P], _P),
+    "ipm_sqp_kernel_launches": ([_P], C.c_int64),
+    "ipm_sqp_last_error": ([_P], C.c_char_p),
+    "ipm_sqp_destroy": ([_P], None),
 }
 EXPORTED = tuple(_sigs)
 

@@ -15,7 +15,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["linalg.cu", "compact.cu", "pcg.cu", "ipmops.cu", "shard.cu", "comm.cu", "ipm_api.cu"]
+SOURCES = ["linalg.cu", "compact.cu", "pcg.cu", "ipmops.cu", "shard.cu", "comm.cu", "ipm_api.cu", "sqp.cu"]
 
 
 def _stale(out: str, deps) -> bool:
@@ -27,7 +27,7 @@ def _stale(out: str, deps) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> str:
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
-    headers.append(os.path.join(ROOT, "include", "ipm.h"))
+    headers += [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []

@@ -8,7 +8,7 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "ipm.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
 
 
 @pytest.fixture(scope="module")
@@ -20,7 +20,7 @@ def lib():
 
 
 def _declared():
-    txt = open(HEADER).read()
+    txt = "".join(open(h).read() for h in HEADERS)
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(ipm_[a-z0-9_]+)\s*\(", txt)))
 
@@ -103,3 +103,19 @@ def test_partition_validation_before_any_device_work(lib):
     st = lib.ipm_create(C.byref(ctx), C.byref(p), None, None, 0, None)
     assert st == lib.IPM_ERR_INVALID and b"nranks > 1 needs comm_kind" in lib.ipm_last_error(None)
     grp.close()
+
+
+def test_sqp_struct_sizes_match_c(lib, tmp_path):
+    """include/sqp.h structs vs the ctypes mirrors."""
+    src = tmp_path / "sq.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "sqp.h"\nint main(){printf("%zu %zu %zu %zu %zu\\n",'
+                   'sizeof(ipm_dose_nlp), sizeof(ipm_sqp_options), sizeof(ipm_sqp_stats), sizeof(ipm_sqp_trace_rec),'
+                   'offsetof(ipm_sqp_options, h0_floor));return 0;}\n')
+    exe = tmp_path / "sq"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    assert vals == [C.sizeof(lib.ipm_dose_nlp), C.sizeof(lib.ipm_sqp_options), C.sizeof(lib.ipm_sqp_stats),
+                    C.sizeof(lib.ipm_sqp_trace_rec), lib.ipm_sqp_options.h0_floor.offset]
+    o = lib.ipm_sqp_options()
+    lib.ipm_sqp_options_default(C.byref(o))
+    assert o.size == C.sizeof(lib.ipm_sqp_options) and o.max_iter == 50 and o.tol_d == 1e-6 and o.powell == 0.2
