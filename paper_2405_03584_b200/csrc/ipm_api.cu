@@ -211,7 +211,7 @@ void assign_vectors(ipm_ctx *c, const Offsets &o) {
     V.sig_b = nv[k++]; V.Minv = nv[k++]; V.rhs = nv[k++]; V.dx = nv[k++];
     V.ds_lx = nv[k++]; V.ds_ux = nv[k++]; V.dl_lx = nv[k++]; V.dl_ux = nv[k++];
     V.ads_lx = nv[k++]; V.ads_ux = nv[k++]; V.adl_lx = nv[k++]; V.adl_ux = nv[k++];
-    V.pr = nv[k++]; V.pz = nv[k++]; V.pp = nv[k++]; V.py = nv[k++];
+    V.pr = nv[k++]; V.pz = nv[k++]; V.pp = nv[k++]; V.py = nv[k++]; V.pAt = nv[k++];
     int j = 0;
     V.s_lA = mv[j++]; V.s_uA = mv[j++]; V.lam_lA = mv[j++]; V.lam_uA = mv[j++];
     V.r_lA = mv[j++]; V.r_uA = mv[j++]; V.rc_lA = mv[j++]; V.rc_uA = mv[j++]; V.Ax = mv[j++];
@@ -305,7 +305,7 @@ ipm_status pcg_iteration_sharded(ipm_ctx *ctx) {
     TRY(xcombine(ctx, X_PCG_ALPHA));
     launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, ctx->st);
     TRY(xcombine(ctx, X_PCG_UPDATE));
-    ctx->launches += 3 + (P.m > 0 ? 1 : 0);
+    ctx->launches += 3 + (P.m > 0 ? 2 : 0);
     CKL();
     return IPM_OK;
 }
@@ -387,14 +387,14 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
                     launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork);
                 TRY(sync_scalars(ctx));
                 DBG("  host batch: it=%lld rr=%.3e done=%lld\n", (long long)ctx->hsc->it, ctx->hsc->rr, (long long)ctx->hsc->done);
-                ctx->launches += 16 * (3 + (P.m > 0 ? 1 : 0));
+                ctx->launches += 16 * (3 + (P.m > 0 ? 2 : 0));
                 if (ctx->hsc->done) break;
             }
         }
         const Scalars &h = *ctx->hsc;
         DBG("pcg round %d: it=%lld rr=%.3e tol2=%.3e done=%lld breakdown=%lld rho=%.3e pKp=%.3e\n", round,
             (long long)h.it, h.rr, h.tol2, (long long)h.done, (long long)h.breakdown, h.rho, h.pKp);
-        if (graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * (3 + (P.m > 0 ? 1 : 0));
+        if (graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * (3 + (P.m > 0 ? 2 : 0));
         it_prev = h.it;
         if (h.breakdown) {
             out.iters = h.it;
@@ -1143,7 +1143,7 @@ IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, doub
     float t = 0.f;
     CK(cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]));
     *ms = (double)t / reps;
-    ctx->launches += (int64_t)(reps + 1) * (what == 2 ? (3 + (P.m > 0)) : 1);
+    ctx->launches += (int64_t)(reps + 1) * (what == 2 ? (3 + 2 * (P.m > 0)) : 1);
     return IPM_OK;
 }
 

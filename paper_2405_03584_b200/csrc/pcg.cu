@@ -230,8 +230,7 @@ k_pcg_p(int n, const double *__restrict__ z, double *__restrict__ p, const doubl
 template <int G>
 __global__ void __launch_bounds__(kBlock)
 k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
-             const double *__restrict__ p, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol,
-             const double *__restrict__ ATval, const double *__restrict__ t, double *__restrict__ x,
+             const double *__restrict__ p, const double *__restrict__ pAt, double *__restrict__ x,
              double *__restrict__ r, double *__restrict__ z, const double *__restrict__ Minv,
              double *__restrict__ p1, double *__restrict__ p2, Scalars *sc, cudaGraphConditionalHandle h,
              int use_cond, AugArgs ag) {
@@ -269,23 +268,20 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
         const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
         const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         // lane 0's row operands are independent of the reduction: load them first
-        double pi = 0.0, sbi = 0.0, xi = 0.0, ri0 = 0.0, mi = 0.0;
+        double pi = 0.0, sbi = 0.0, xi = 0.0, ri0 = 0.0, mi = 0.0, ati = 0.0;
         if (gl == 0) {
             pi = p[i];
             sbi = sigb[i];
             xi = x[i];
             ri0 = r[i];
             mi = Minv[i];
+            if (pAt != nullptr) ati = pAt[i];
         }
         double s = 0.0;
         for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
-        if (t != nullptr) {
-            const int64_t e = ATrp[i + 1];
-            for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
-        }
         s = group_sum<G>(s);
         if (act && gl == 0) {
-            const double yi = fma(sbi, pi, s);
+            const double yi = fma(sbi, pi, s + ati);   // (H p)_i + sigma_b p_i + (A^T t)_i
             x[i] = fma(alpha, pi, xi);
             const double ri = fma(-alpha, yi, ri0);
             r[i] = ri;
@@ -429,14 +425,47 @@ void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
                                                                                 sc, aug_args(P, V));
 }
 
+// (A^T t)_i for the local rows, a G-lane group per row of the stored transpose.  Runs on the
+// SpMV side branch right after t is formed, so the update kernel reads one value per row
+// instead of gathering over A^T while the GEMV's result waits.
+template <int G>
+__global__ void __launch_bounds__(kBlock)
+k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, const double *__restrict__ ATval,
+        const double *__restrict__ t, double *__restrict__ out, const Scalars *sc) {
+    if (sc->done) return;
+    const int gl = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;
+        double s = 0.0;
+        const int64_t e = ATrp[i + 1];
+        for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
+        s = group_sum<G>(s);
+        if (act && gl == 0) out[i] = s;
+    }
+}
+
+static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st) {
+    if (P.m == 0 || P.n == 0) return;
+    const int g = grid_for(P.n, kBlock / G);
+    switch (G) {
+        case 4: k_spmvT<4><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        case 8: k_spmvT<8><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        case 16: k_spmvT<16><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        default: k_spmvT<32><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+    }
+}
+
 static void launch_update_g(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x,
                             cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
     const int ug = grid_for(P.n, kBlock / G);
-    const double *t = (P.m > 0) ? V.pt : nullptr;
+    const double *pAt = (P.m > 0) ? V.pAt : nullptr;
     const AugArgs ag = aug_args(P, V);
 #define IPM_UPD(GG)                                                                                              \
-    k_pcg_update<GG><<<ug, kBlock, 0, st>>>(P.n, ncb, V.ypart, V.sig_b, V.pp, P.ATrp, P.ATcol, P.ATval, t, x, V.pr, \
-                                            V.pz, V.Minv, V.part[5], V.part[6], sc, h, use_cond, ag)
+    k_pcg_update<GG><<<ug, kBlock, 0, st>>>(P.n, ncb, V.ypart, V.sig_b, V.pp, pAt, x, V.pr, V.pz, V.Minv,         \
+                                            V.part[5], V.part[6], sc, h, use_cond, ag)
     switch (G) {
         case 4: IPM_UPD(4); break;
         case 8: IPM_UPD(8); break;
@@ -446,15 +475,18 @@ static void launch_update_g(const Prob &P, const Vecs &V, int G, int ncb, Scalar
 #undef IPM_UPD
 }
 
+// sharded path: t is complete (replicated on every rank) when this is called
 void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st) {
+    launch_spmvT(P, V, G, sc, st);
     launch_update_g(P, V, G, ncb, sc, x, 0, 0, st);
 }
 
 // the SpMV stage of an iteration: condensed t = sig_c o (A p), or (NEXT-2) the augmented
 // t = 2 sig_c o (A p_x) + p_l - p_u and the middle block rows y_l, y_u
-static void spmv_stage(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
+static void spmv_stage(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st) {
     if (P.aug) launch_spmv_aug(P, V, V.pp, V.ag.pl, V.ag.pu, sc, 1, st);
     else launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
+    launch_spmvT(P, V, G, sc, st);
 }
 
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
@@ -467,10 +499,10 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
     if (par) {
         cudaEventRecord(fork->ev_fork, st);
         cudaStreamWaitEvent(fork->side, fork->ev_fork, 0);
-        spmv_stage(P, V, sc, fork->side);
+        spmv_stage(P, V, G, sc, fork->side);
         cudaEventRecord(fork->ev_join, fork->side);
     } else {
-        spmv_stage(P, V, sc, st);
+        spmv_stage(P, V, G, sc, st);
         if (!use_cond) dstage("spmv", st);
     }
     launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);

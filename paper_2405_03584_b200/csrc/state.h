@@ -105,6 +105,7 @@ struct Vecs {
     double *lamd;                                   // lam_lA - lam_uA scratch (m)
     // PCG
     double *pr, *pz, *pp, *pt, *py;                  // r, z, p (n), t (m), y (n)
+    double *pAt;                                     // A^T t (n), formed on the SpMV branch
     double *ypart;                                   // n x ncb GEMV tile partials
     double *gfull;                                   // sharded: gathered full-length vector (P*chunk)
     double *xloc_all;                                // sharded: allgathered loc[] of all ranks (8*P)
