@@ -179,6 +179,7 @@ def run_ours(args):
     # N > 1: ONE QP row-sharded over the ranks (NCCL allgathers inside libipm),
     # each rank building only its row block of H on its device; --replicas: N independent QPs.
     sharded = (ws > 1 or args.force_shard) and not args.replicas
+    extra = {"use_graph": 0} if args.host_loop else {}
     rows = (0, n)
     if sharded:
         from gen.torch_io import device_hessian
@@ -190,12 +191,12 @@ def run_ours(args):
         def make_qp(tensors):
             uid = (nccl_unique_id() if ws == 1
                    else broadcast_unique_id(nccl_unique_id, rank, dist.broadcast_object_list))
-            return QP(device=dev, shard=nccl_shard(rank, ws, uid), **tensors)
+            return QP(device=dev, shard=nccl_shard(rank, ws, uid), **extra, **tensors)
     else:
         t = problem_tensors(q, dev)
 
         def make_qp(tensors):
-            return QP(device=dev, **tensors)
+            return QP(device=dev, **extra, **tensors)
     torch.cuda.synchronize()
     qp = make_qp(t)
     stream = qp.stream
@@ -211,6 +212,7 @@ def run_ours(args):
     clocks.start()
     stats = []
     launches0 = qp.kernel_launches()
+    kt0 = qp.kernel_timer()
     torch.cuda.synchronize()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -224,6 +226,8 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     launches = qp.kernel_launches() - launches0
+    kt1 = qp.kernel_timer()
+    kt_ms, kt_n = kt1[0] - kt0[0], kt1[1] - kt0[1]
     t_s = e0.elapsed_time(e1) / 1e3
     tt = torch.tensor([t_s], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -236,7 +240,10 @@ def run_ours(args):
 
     # --- roofline of the dominant kernel (the PCG GEMV), CUDA events on our stream -------
     info = qp.info()
-    gemv_ms = qp.profile("gemv", reps=10 if n >= 10000 else 50)
+    gemv_iso_ms = qp.profile("gemv", reps=10 if n >= 10000 else 50)
+    # live: the dominant kernel's own average launch duration over the timed region
+    # (device %globaltimer from its first CTA start to its last CTA end, summed in-kernel)
+    gemv_ms = kt_ms / kt_n if kt_n > 0 else gemv_iso_ms
     pcg_iter_ms = qp.profile("pcg_iter", reps=10 if n >= 10000 else 50)
     ncb = info["ncb"]
     if info["gemv_kernel"] == 3:
@@ -339,8 +346,12 @@ def run_ours(args):
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "algorithmic_bytes_per_launch": gemv_bytes,
                          "dense_equivalent_GBps": effective,
-                         "launch_ms": gemv_ms, "peak_source": peak_src,
-                         "timing": "CUDA events on the library stream, back-to-back launches after the timed region"},
+                         "launch_ms": gemv_ms, "launches_timed": int(kt_n), "peak_source": peak_src,
+                         "share_of_step": kt_ms / (t_max * 1e3) if kt_n > 0 else None,
+                         "isolated_launch_ms": gemv_iso_ms,
+                         "timing": ("live: in-kernel %globaltimer (first CTA start to last CTA end) summed over "
+                                    "every launch in the timed region, on the library stream"
+                                    if kt_n > 0 else "CUDA events, back-to-back launches after the timed region")},
             "cpu_baseline": cpu,
             "e2e": {"value": (1 if sharded else ws) * args.steps / float(te.item()), "unit": "QP/s",
                     "h2d_bytes_per_step": int(h2d),
@@ -365,6 +376,9 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N>1: N independent QPs instead of one sharded QP")
     ap.add_argument("--force-shard", action="store_true", help="N=1: run the NCCL row-sharded code path")
     ap.add_argument("--no-extra", action="store_true", help="skip the C1/C2 context timings")
+    ap.add_argument("--host-loop", action="store_true",
+                    help="profiling only: drive the PCG from the host (batches of 16) instead of the conditional-"
+                         "WHILE graph, whose kernel nodes ncu cannot profile one by one")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

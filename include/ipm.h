@@ -241,6 +241,12 @@ ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, double *ms_host
  * executed node); used by bench.py's gpu_launches. */
 int64_t ipm_kernel_launches(const ipm_ctx *ctx);
 
+/* Live device-side timing of the PCG operator kernel (the dominant GEMV / SYMV in PCG
+ * mode): cumulative duration in ms (first CTA start to last CTA end, %globaltimer) and
+ * number of timed launches since create, read on ctx's stream (synchronises it).
+ * bench.py differences two reads around its timed region.  Host pointers. */
+ipm_status ipm_kernel_timer(ipm_ctx *ctx, double *ms_total_host, int64_t *launches_host);
+
 /* Context-local message of the last failure (or the last create failure for NULL). */
 const char *ipm_last_error(const ipm_ctx *ctx);
 void ipm_destroy(ipm_ctx *ctx);

@@ -92,6 +92,25 @@ __device__ __forceinline__ bool last_block(unsigned int *counter) {
     return am_last;
 }
 
+// Device-side launch timer (ns, %globaltimer): the PCG's dominant kernel records the
+// earliest CTA start and, in its last CTA, adds (end - start) to a running sum, so bench.py
+// reads the kernel's average launch duration over the timed region without splitting the
+// captured graph (CUDA events cannot bracket a node inside a conditional WHILE body).
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void ktimer_start(unsigned long long *neg) {
+    if (threadIdx.x == 0) atomicMax(neg, ~gtimer_ns());
+}
+__device__ __forceinline__ void ktimer_stop(unsigned long long *neg, unsigned long long *ns, unsigned long long *cnt) {
+    const unsigned long long e = gtimer_ns();
+    const unsigned long long s = ~atomicExch(neg, 0ull);
+    if (e > s) *ns += e - s;
+    *cnt += 1;
+}
+
 // Fixed-order sum of `cnt` partials by one block (all threads get it).
 __device__ __forceinline__ double sum_partials(const double *part, int cnt, double *sh) {
     double v = 0.0;

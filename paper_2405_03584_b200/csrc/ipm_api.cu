@@ -359,7 +359,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
         TRY(xcombine(ctx, X_PCG_RESTART));
     }
     ctx->have_dx = true;
-    const bool small = !ctx->sharded && !P.aug && P.n <= kSmallN && ctx->opt.use_graph;
+    const bool small = !ctx->sharded && !P.aug && !P.hess_compact && P.n <= kSmallN && ctx->opt.use_graph;
     const bool graph = ctx->opt.use_graph && !ctx->sharded && !small;
     if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
@@ -888,6 +888,13 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=3 needs an unsharded, exactly symmetric H with even ldh");
         if (gk == 2 && !bulk_ok) return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=2 needs even ldh and 16-byte aligned H");
         P.gemv_sym = sym ? 1 : 0;
+        P.sym_keep = 0;
+        if (sym) {
+            const char *e = getenv("IPM_SYM_KEEP_MB");      // experiment: L2-resident share of H
+            const double mb = e ? atof(e) : 0.0;
+            const int64_t tiles = (int64_t)(mb * 1048576.0 / (8.0 * kSymB * kSymB));
+            P.sym_keep = (int)(tiles / std::max(1, gemv_bulk_grid()));
+        }
         P.gemv_bulk = (!sym && !P.hess_compact && (gk == 0 || gk == 2) && bulk_ok) ? 1 : 0;
         P.gemv_bulk_grid = gemv_bulk_grid();
         ctx->ncb = P.hess_compact ? 1 : (sym ? sym_ncb((int)p->n) : gemv_ncb((int)p->n));
@@ -1161,6 +1168,16 @@ IPM_EXPORT ipm_status ipm_get_info(const ipm_ctx *ctx, ipm_info *info) {
 }
 
 IPM_EXPORT int64_t ipm_kernel_launches(const ipm_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+IPM_EXPORT ipm_status ipm_kernel_timer(ipm_ctx *ctx, double *ms_total, int64_t *launches) {
+    if (!ctx || !ms_total || !launches) return fail(ctx, IPM_ERR_INVALID, "bad argument");
+    unsigned long long v[2] = {0, 0};
+    CK(cudaMemcpyAsync(v, &ctx->sc->kt_ns, sizeof v, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    *ms_total = (double)v[0] * 1e-6;
+    *launches = (int64_t)v[1];
+    return IPM_OK;
+}
 
 IPM_EXPORT const char *ipm_last_error(const ipm_ctx *ctx) {
     return ctx ? ctx->err.c_str() : g_create_error.c_str();

@@ -38,6 +38,7 @@ k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
     __shared__ __align__(16) double ps[kGemvCW];
     __shared__ double red[kGemvThreads / 32];
     if (MODE == 1 && sc->done) return;
+    if (MODE == 1) ktimer_start(&sc->kt_neg);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nrb = (nrows + kGemvRB - 1) / kGemvRB;
     const int64_t ntiles = (int64_t)nrb * ncb;
@@ -112,6 +113,7 @@ k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
+            if (MODE == 1) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
             if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
             // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
@@ -207,6 +209,7 @@ k_gemv_bulk(const double *__restrict__ H, int64_t ldh, int nrows, int ncols, con
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[kBulkThreads / 32];
     if (MODE == 1 && sc->done) return;
+    if (MODE == 1) ktimer_start(&sc->kt_neg);
     double *stages = reinterpret_cast<double *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kBulkStages * kBulkStageDoubles * 8);
     uint64_t *empty = full + kBulkStages;
@@ -292,6 +295,7 @@ k_gemv_bulk(const double *__restrict__ H, int64_t ldh, int nrows, int ncols, con
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
+            if (MODE == 1) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
             if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
             // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
@@ -395,11 +399,12 @@ template <int MODE>
 __global__ void __launch_bounds__(kSymThreads, 1)
 k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__restrict__ p,
             const double *__restrict__ pdot, double *__restrict__ ypart, int nb, double *__restrict__ dpart,
-            Scalars *sc, int cid) {
+            Scalars *sc, int cid, int keep) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[kSymThreads / 32];
     __shared__ double colbuf[kSymB];                  // row-half-1 column sums of the current tile
     if (MODE == 1 && sc->done) return;
+    if (MODE == 1) ktimer_start(&sc->kt_neg);
     double *stages = reinterpret_cast<double *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kSymStages * kSymStageDoubles * 8);
     uint64_t *empty = full + kSymStages;
@@ -438,7 +443,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                     double *sPI = sPJ + kSymB;
                     // one 2-D TMA per strip: kSymSR x kSymB box (OOB rows/cols zero-filled, full box bytes)
                     mbar_expect_tx(&full[stage], (uint32_t)((kSymSR * kSymB + cwb + rb) * 8));
-                    tma_2d_g2s(sH, &tmap, J * kSymB, I * kSymB + s0, &full[stage], pol_h);
+                    tma_2d_g2s(sH, &tmap, J * kSymB, I * kSymB + s0, &full[stage], (t - t0 < keep) ? pol_p : pol_h);
                     bulk_g2s(sPJ, p + (int64_t)J * kSymB, (uint32_t)(cwb * 8), &full[stage], pol_p);
                     bulk_g2s(sPI, p + (int64_t)I * kSymB + s0, (uint32_t)(rb * 8), &full[stage], pol_p);
                     if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
@@ -545,6 +550,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
+            if (MODE == 1) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
             if (sc->sharded) sc->loc[1] = tot;
             // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
@@ -562,9 +568,9 @@ void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double
     const int nb = sym_ncb(P.n);
     const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(P.tmap_sym);
     if (mode == 1)
-        k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+        k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid, P.sym_keep);
     else
-        k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid);
+        k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid, P.sym_keep);
 }
 
 // Exact-symmetry check at create (the symmetric GEMV is only used when H == H^T bitwise).

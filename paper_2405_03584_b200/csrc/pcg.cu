@@ -458,8 +458,23 @@ static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaS
     }
 }
 
-static void launch_update_g(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x,
+// Lanes per row of the update kernel: it sums the ncb GEMV partials of each row (A^T t now
+// arrives precomputed from the SpMV branch), so the group size follows ncb alone.
+static int update_group(int ncb) {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("IPM_UPD_G");
+        env = e ? atoi(e) : 0;
+    }
+    if (env == 4 || env == 8 || env == 16 || env == 32) return env;
+    if (ncb <= 16) return 4;
+    if (ncb <= 64) return 8;
+    return 16;
+}
+
+static void launch_update_g(const Prob &P, const Vecs &V, int /*G*/, int ncb, Scalars *sc, double *x,
                             cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
+    const int G = update_group(ncb);
     const int ug = grid_for(P.n, kBlock / G);
     const double *pAt = (P.m > 0) ? V.pAt : nullptr;
     const AugArgs ag = aug_args(P, V);

@@ -47,6 +47,10 @@ struct Scalars {
     int64_t sharded;
     double loc[8];
     unsigned int counters[kNumCounters];
+    // --- live launch timing of the PCG operator kernel (bench.py roofline) ---------------
+    // kt_neg = max over CTAs of ~(start %globaltimer) (so 0 = unset), reset by the last CTA,
+    // which adds (its end - earliest start) to kt_ns and counts the launch.
+    unsigned long long kt_neg, kt_ns, kt_count;
 };
 
 // Combine stages of k_xcombine (shard.cu).
@@ -76,6 +80,7 @@ struct Prob {
     int gemv_bulk;         // 1: use the TMA-bulk GEMV (k_gemv_bulk) with grid gemv_bulk_grid
     int gemv_bulk_grid;
     int gemv_sym;          // 1: symmetric upper-triangle TMA-bulk GEMV (k_symv_bulk)
+    int sym_keep;          // leading tiles of each CTA's range loaded with an L2 evict_last policy
     int ncb;               // column blocks of the ypart[row][cb] layout of the chosen GEMV
     const void *tmap_sym;  // host copy of the CUtensorMap over H (16 x 256 fp64 boxes)
     // compact quasi-Newton Hessian H = diag(h0) + U diag(w) U^T (compact.cu)

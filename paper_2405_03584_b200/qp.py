@@ -192,6 +192,12 @@ class QP:
     def kernel_launches(self) -> int:
         return int(L.ipm_kernel_launches(self.ctx))
 
+    def kernel_timer(self) -> tuple:
+        """(cumulative ms, launches) of the PCG operator kernel, timed on the device."""
+        ms, cnt = C.c_double(), C.c_int64()
+        L.check(L.ipm_kernel_timer(self.ctx, C.byref(ms), C.byref(cnt)), self.ctx)
+        return ms.value, cnt.value
+
     # ------------------------------------------------------------------ C4
     def set_linear_term(self, g):
         self._g_new = _dev(g, torch.float64, self.device)

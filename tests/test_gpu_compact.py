@@ -39,8 +39,11 @@ def test_compact_apply_and_diag(n, m, r):
     assert np.max(np.abs(d - okkt.jacobi_diag(q.H, q.A_dense(), sb, sc)) / d) <= 1e-13
 
 
-def test_compact_ipm_matches_oracle():
-    q = planted_qp(1500, 300, density=0.02, rank=40, seed=17, rows="vmat", var="box")
+@pytest.mark.parametrize("n,m,r", [(1500, 300, 40), (120, 30, 9)])
+def test_compact_ipm_matches_oracle(n, m, r):
+    """(120, 30): n below the single-CTA PCG threshold, which needs the dense H and must not
+    be chosen for a compact Hessian (regression: it read H = NULL)."""
+    q = planted_qp(n, m, density=0.02 if n > 1000 else 0.15, rank=r, seed=17, rows="vmat", var="box")
     qp = _compact_qp(q)
     assert qp.solve() == "ok"
     ref = solve(Problem.from_data(q))
