@@ -250,8 +250,9 @@ def run_ours(args):
         # symmetric GEMV streams the upper block triangle of H (kSymB = 256 blocks, diagonal
         # blocks whole): algorithmic bytes = 8 * sum over tiles I <= J of rows_I * cols_J
         B = 256
-        sizes = [min(B, n - i * B) for i in range(ncb)]
-        tri = sum(sizes[i] * sizes[j] for i in range(ncb) for j in range(i, ncb))
+        nb = (n + B - 1) // B            # ncb = nb + the carry slots of the strip-balanced split
+        sizes = [min(B, n - i * B) for i in range(nb)]
+        tri = sum(sizes[i] * sizes[j] for i in range(nb) for j in range(i, nb))
         gemv_bytes = 8.0 * tri + 8.0 * n + 8.0 * n * ncb
         kname = "k_symv_bulk<1> (symmetric upper-triangle GEMV, 2-D TMA, p^T H p fused)"
     else:

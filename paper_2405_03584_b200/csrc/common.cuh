@@ -111,6 +111,26 @@ __device__ __forceinline__ void ktimer_stop(unsigned long long *neg, unsigned lo
     *cnt += 1;
 }
 
+// Grid-wide barrier for cooperatively launched kernels (all CTAs co-resident): arrival
+// counter + generation word.  The generation is read BEFORE arriving, so the last arrival's
+// increment cannot be missed; fences order every CTA's prior global writes before release.
+__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int g = *(volatile unsigned int *)gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *(volatile unsigned int *)count = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*(volatile unsigned int *)gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // Fixed-order sum of `cnt` partials by one block (all threads get it).
 __device__ __forceinline__ double sum_partials(const double *part, int cnt, double *sh) {
     double v = 0.0;

@@ -74,7 +74,7 @@ struct Offsets {
     size_t nvec[40];
     size_t mvec[40];
     size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad, gfull, xloc_all;
-    size_t ch0, cw, cs, cspart, chpart;
+    size_t ch0, cw, cs, cspart, chpart, symr;
     int n_nvec, n_mvec;
     int nchunk;
 };
@@ -97,7 +97,10 @@ Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks
     o.sc = L.take(sizeof(Scalars));
     for (int i = 0; i < kNVec; ++i) o.nvec[i] = L.take(sizeof(double) * (std::max<int64_t>(chunk, 1) + 2));
     for (int i = 0; i < kMVec; ++i) o.mvec[i] = L.take(sizeof(double) * std::max<int64_t>(m, 1));
-    o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) * std::max(gemv_ncb((int)ncols), sym_ncb((int)ncols)));
+    const int symK = (nranks == 1) ? sym_partition((int)ncols, gemv_bulk_grid(), nullptr) : 0;
+    o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) *
+                     std::max(gemv_ncb((int)ncols), sym_ncb((int)ncols) + symK));
+    o.symr = L.take(sizeof(SymRange) * (size_t)gemv_bulk_grid());
     o.part = L.take(sizeof(double) * kMaxPartials * 8);
     o.ATrp = L.take(sizeof(int64_t) * (nloc + 1));
     o.ATcol = L.take(sizeof(int) * std::max<int64_t>(nnz_loc, 1));
@@ -139,6 +142,7 @@ struct ipm_ctx {
     cudaGraphExec_t gexec = nullptr;
     cudaGraphConditionalHandle handle = 0;
     bool graph_ready = false;
+    bool fused_p = false;        // PCG iterations use k_pcg_update_fp (p-update fused, cooperative)
     // state
     bool have_iterate = false;   // V holds a valid iterate (after a solve or set_iterate)
     bool user_iterate = false;   // set_iterate called: next solve starts from it
@@ -324,7 +328,7 @@ ipm_status build_graph(ipm_ctx *ctx) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(ctx->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle, 1, ctx->cap,
-                         &ctx->fork);
+                         &ctx->fork, ctx->fused_p);
     cudaGraph_t captured = nullptr;
     CK(cudaStreamEndCapture(ctx->cap, &captured));
     CK(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
@@ -364,7 +368,13 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
     if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
     int64_t it_prev = 0;
+    const int per_it = (ctx->fused_p ? 2 : 3) + (P.m > 0 ? 2 : 0);   // kernels per PCG iteration
     for (int round = 0;; ++round) {
+        if (ctx->fused_p && !small) {
+            launch_pcg_p(P, V, ctx->sc, ctx->st);           // p = z after the (re)start; S_b
+            ctx->launches += 1;
+            CKL();
+        }
         if (small) {
             launch_pcg_small(P, V, ctx->sc, V.dx, ctx->st);
             ctx->launches += 1;
@@ -384,17 +394,18 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
             // host-driven fallback: batches of 16 iterations with device-side early exit
             for (;;) {
                 for (int b = 0; b < 16; ++b)
-                    launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork);
+                    launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork,
+                                         ctx->fused_p);
                 TRY(sync_scalars(ctx));
                 DBG("  host batch: it=%lld rr=%.3e done=%lld\n", (long long)ctx->hsc->it, ctx->hsc->rr, (long long)ctx->hsc->done);
-                ctx->launches += 16 * (3 + (P.m > 0 ? 2 : 0));
+                ctx->launches += 16 * per_it;
                 if (ctx->hsc->done) break;
             }
         }
         const Scalars &h = *ctx->hsc;
         DBG("pcg round %d: it=%lld rr=%.3e tol2=%.3e done=%lld breakdown=%lld rho=%.3e pKp=%.3e\n", round,
             (long long)h.it, h.rr, h.tol2, (long long)h.done, (long long)h.breakdown, h.rho, h.pKp);
-        if (graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * (3 + (P.m > 0 ? 2 : 0));
+        if (graph) ctx->launches += std::max<int64_t>(1, h.it - it_prev) * per_it;
         it_prev = h.it;
         if (h.breakdown) {
             out.iters = h.it;
@@ -890,20 +901,39 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         P.gemv_sym = sym ? 1 : 0;
         P.sym_keep = 0;
         if (sym) {
-            const char *e = getenv("IPM_SYM_KEEP_MB");      // experiment: L2-resident share of H
-            const double mb = e ? atof(e) : 0.0;
-            const int64_t tiles = (int64_t)(mb * 1048576.0 / (8.0 * kSymB * kSymB));
-            P.sym_keep = (int)(tiles / std::max(1, gemv_bulk_grid()));
+            // an upper block triangle that fits in L2 (C2: 100 MB of 126 MB) is loaded with an
+            // evict_last policy so it stays resident across PCG iterations; larger H streams
+            // evict_first (measured: no gain from a resident share at C3, -8% GEMV time at C2)
+            const double tri = 4.0 * (double)p->n * (double)(p->n + kSymB);
+            const char *e = getenv("IPM_SYM_KEEP_MB");      // experiment override
+            const double mb = e ? atof(e) : (tri <= 100.0 * 1048576.0 ? 1e9 : 0.0);
+            const double tiles = mb * 1048576.0 / (8.0 * kSymB * kSymB);
+            P.sym_keep = (int)std::min(1e9, tiles / std::max(1, gemv_bulk_grid())) + (mb > 0 ? 1 : 0);
         }
         P.gemv_bulk = (!sym && !P.hess_compact && (gk == 0 || gk == 2) && bulk_ok) ? 1 : 0;
         P.gemv_bulk_grid = gemv_bulk_grid();
-        ctx->ncb = P.hess_compact ? 1 : (sym ? sym_ncb((int)p->n) : gemv_ncb((int)p->n));
+        int symK = 0;
+        if (sym) {                  // strip-balanced ranges of the symmetric GEMV (kernels.h)
+            std::vector<SymRange> rg((size_t)P.gemv_bulk_grid);
+            symK = sym_partition((int)p->n, P.gemv_bulk_grid, rg.data());
+            SymRange *d = reinterpret_cast<SymRange *>(ctx->ws + o.symr);
+            CK(cudaMemcpyAsync(d, rg.data(), sizeof(SymRange) * rg.size(), cudaMemcpyHostToDevice, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            P.sym_ranges = d;
+        }
+        ctx->ncb = P.hess_compact ? 1 : (sym ? sym_ncb((int)p->n) + symK : gemv_ncb((int)p->n));
         P.ncb = ctx->ncb;
         if (ctx->opt.pcg_system != 0 && ctx->opt.pcg_system != 1) return fail(ctx, IPM_ERR_INVALID, "unknown pcg_system");
         if (ctx->opt.pcg_system == 1 && ctx->sharded)
             return fail(ctx, IPM_ERR_INVALID, "pcg_system = 1 (doubly augmented) is unsharded only");
         P.aug = (ctx->opt.pcg_system == 1 && p->m > 0) ? 1 : 0;
         ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
+        {   // fused update + p (cooperative grid barrier): single-GPU condensed PCG
+            int coop = 0;
+            CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
+            const char *e = getenv("IPM_FUSED_P");
+            ctx->fused_p = coop && !ctx->sharded && !P.aug && !(e && atoi(e) == 0);
+        }
         DBG("create: n=%lld m=%lld nnz=%lld gemv=%s ncb=%d G=%d sharded=%d\n", (long long)p->n, (long long)p->m,
             (long long)p->nnz, sym ? "symmetric-bulk" : (P.gemv_bulk ? "bulk" : "ldg"), ctx->ncb, ctx->G,
             (int)ctx->sharded);
@@ -1131,12 +1161,14 @@ IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, doub
     const Vecs &V = ctx->V;
     CK(cudaMemsetAsync(&ctx->sc->done, 0, sizeof(int64_t), ctx->st));
     CK(cudaMemsetAsync(&ctx->sc->it_rs, 0, sizeof(int64_t), ctx->st));
+    if (what == 2 && ctx->fused_p) launch_pcg_p(P, V, ctx->sc, ctx->st);
     auto one = [&]() {
         // what 0: the PCG GEMV's full work (tiles + fused p^T H p) without its done/alpha epilogue
         if (what == 0) launch_gemv(P, V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV_PCG, ctx->st);
         else if (what == 1 && P.aug) launch_spmv_aug(P, V, V.pp, V.ag.pl, V.ag.pu, ctx->sc, 1, ctx->st);
         else if (what == 1) launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
-        else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork);
+        else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork,
+                                  ctx->fused_p);
     };
     one();  // warm-up
     CK(cudaEventRecord(ctx->ev[2], ctx->st));

@@ -17,6 +17,23 @@ constexpr int kGemvCW = 1024;       // columns per GEMV tile (8 KB of the vector
 inline int gemv_ncb(int ncols) { return (ncols + kGemvCW - 1) / kGemvCW; }
 constexpr int kSymB = 256;          // symmetric GEMV: square B x B blocks of H
 inline int sym_ncb(int n) { return (n + kSymB - 1) / kSymB; }
+constexpr int kSymSR = 32;          // symmetric GEMV: rows per TMA strip (pipeline stage)
+
+// Strip-balanced work split of the symmetric GEMV.  The strips (kSymSR rows x kSymB columns)
+// of the upper block triangle, in tile order (row-major over tiles I <= J), are cut into
+// `grid` contiguous ranges of equal length, so no CTA streams more than one strip (64 KB)
+// above the average.  A range may start inside a tile: that CTA's column partial of the
+// tile's first (partial) visit goes to an extra "carry" slot nb + carry of the ypart row
+// instead of slot I (which the tile's owner, the CTA holding its strip 0, writes), so every
+// slot is still written by exactly one CTA and the consumers' fixed-order sums stay
+// deterministic.  Returns the number of carry slots K (ypart stride = nb + K).
+struct SymRange {
+    int t0, s0;     // first tile (upper-triangle row-major index) and first strip in it
+    int t1, s1;     // end: tile t1, strip s1 (exclusive); s1 == 0 means the range ends at tile t1
+    int carry;      // carry slot of the head partial tile, -1 if none
+    int pad[3];
+};
+int sym_partition(int n, int grid, SymRange *out /* grid entries or nullptr */);
 
 // linalg.cu
 void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb,
@@ -30,8 +47,11 @@ bool make_sym_tensor_map(const Prob &P, void *out128);   // CUtensorMap (128 B, 
 int gemv_bulk_grid();
 void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb, double *dpart,
                       Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
+// max_grid: the PCG's side-branch launch caps the grid at one CTA per SM so the SpMV stage
+// co-resides with the one-CTA-per-SM symmetric GEMV instead of delaying its CTAs
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
-                 Scalars *sc, int mode, int check_done, cudaStream_t st);
+                 Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid = kMaxGrid);
+int num_sms();
 // NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,
 // yu = -A px + D_u pu (masked); mode 1 (PCG): done check + S_c = a.t + pl.yl + pu.yu
 void launch_spmv_aug(const Prob &P, const Vecs &V, const double *px, const double *pl, const double *pu, Scalars *sc,
@@ -63,7 +83,8 @@ struct Fork {  // side stream + events for the SpMV || GEMV branch of a PCG iter
     cudaEvent_t ev_fork, ev_join;
 };
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
-                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork);
+                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork,
+                          bool fused_p = false);
 void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
 constexpr int kSmallN = 256;        // single-CTA PCG loop below this size (launch-latency bound)

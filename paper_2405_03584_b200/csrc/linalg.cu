@@ -22,6 +22,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "state.h"
@@ -340,7 +343,6 @@ void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double
 // the tile and accumulates its column part over the strips in a register; warp w reduces
 // rows w and w+8 of each strip.  Tiles (row-major over the upper triangle) are split among
 // the persistent CTAs as contiguous ranges.
-constexpr int kSymSR = 32;
 constexpr int kSymStages = 3;
 constexpr int kSymConsumers = 16;                 // consumer warps (2 per strip row pair)
 constexpr int kSymThreads = 32 * (kSymConsumers + 1);
@@ -398,8 +400,8 @@ bool make_sym_tensor_map(const Prob &P, void *out) {
 template <int MODE>
 __global__ void __launch_bounds__(kSymThreads, 1)
 k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__restrict__ p,
-            const double *__restrict__ pdot, double *__restrict__ ypart, int nb, double *__restrict__ dpart,
-            Scalars *sc, int cid, int keep) {
+            const double *__restrict__ pdot, double *__restrict__ ypart, int nb, int ldy,
+            const SymRange *__restrict__ ranges, double *__restrict__ dpart, Scalars *sc, int cid, int keep) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[kSymThreads / 32];
     __shared__ double colbuf[kSymB];                  // row-half-1 column sums of the current tile
@@ -417,12 +419,11 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int64_t ntiles = (int64_t)nb * (nb + 1) / 2;
-    const int64_t t0 = ntiles * blockIdx.x / gridDim.x;
-    const int64_t t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
+    const SymRange rg = ranges[blockIdx.x];
+    const int tlast = rg.s1 > 0 ? rg.t1 : rg.t1 - 1;     // last tile touched (inclusive)
     double dacc = 0.0;
     int I = 0, J = 0;
-    if (t0 < t1) sym_locate(t0, nb, I, J);
+    if (rg.t0 <= tlast) sym_locate(rg.t0, nb, I, J);
     if (warp == kSymConsumers) {
         if (lane == 0) {
             uint64_t pol_h, pol_p;
@@ -430,11 +431,14 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_p));
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t t = t0; t < t1; ++t) {
+            for (int t = rg.t0; t <= tlast; ++t) {
                 const int rowsI = min(kSymB, n - I * kSymB);
                 const int colsJ = min(kSymB, n - J * kSymB);
                 const int cwb = (colsJ + 1) & ~1;
-                for (int s0 = 0; s0 < rowsI; s0 += kSymSR) {
+                const int sa = (t == rg.t0) ? rg.s0 : 0;
+                const int sb = (t == rg.t1) ? rg.s1 : (rowsI + kSymSR - 1) / kSymSR;
+                for (int sidx = sa; sidx < sb; ++sidx) {
+                    const int s0 = sidx * kSymSR;
                     const int rows = min(kSymSR, rowsI - s0);
                     const int rb = (rows + 1) & ~1;
                     mbar_wait(&empty[stage], phase ^ 1u);
@@ -443,7 +447,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                     double *sPI = sPJ + kSymB;
                     // one 2-D TMA per strip: kSymSR x kSymB box (OOB rows/cols zero-filled, full box bytes)
                     mbar_expect_tx(&full[stage], (uint32_t)((kSymSR * kSymB + cwb + rb) * 8));
-                    tma_2d_g2s(sH, &tmap, J * kSymB, I * kSymB + s0, &full[stage], (t - t0 < keep) ? pol_p : pol_h);
+                    tma_2d_g2s(sH, &tmap, J * kSymB, I * kSymB + s0, &full[stage], (t - rg.t0 < keep) ? pol_p : pol_h);
                     bulk_g2s(sPJ, p + (int64_t)J * kSymB, (uint32_t)(cwb * 8), &full[stage], pol_p);
                     bulk_g2s(sPI, p + (int64_t)I * kSymB + s0, (uint32_t)(rb * 8), &full[stage], pol_p);
                     if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
@@ -462,18 +466,21 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
         const int h = threadIdx.x / kSymB;
         int stage = 0;
         uint32_t phase = 0;
-        for (int64_t t = t0; t < t1; ++t) {
+        for (int t = rg.t0; t <= tlast; ++t) {
             const int rowsI = min(kSymB, n - I * kSymB);
             const int colsJ = min(kSymB, n - J * kSymB);
             const bool diag = (I == J);
+            const int sa = (t == rg.t0) ? rg.s0 : 0;
+            const int sb = (t == rg.t1) ? rg.s1 : (rowsI + kSymSR - 1) / kSymSR;
             double ce = 0.0, co = 0.0, pj_c = 0.0;
-            for (int s0 = 0; s0 < rowsI; s0 += kSymSR) {
+            for (int sidx = sa; sidx < sb; ++sidx) {
+                const int s0 = sidx * kSymSR;
                 const int rows = min(kSymSR, rowsI - s0);
                 mbar_wait(&full[stage], phase);
                 const double *sH = stages + (size_t)stage * kSymStageDoubles;
                 const double *sPJ = sH + kSymSR * kSymB;
                 const double *sPI = sPJ + kSymB;
-                if (s0 == 0 && c < colsJ) pj_c = sPJ[c];
+                if (sidx == sa && c < colsJ) pj_c = sPJ[c];
                 // row part: rows warp + 16 q (q < kSymRW) of the strip (OOB rows are zero-filled)
                 const double2 *pv = reinterpret_cast<const double2 *>(sPJ);
                 double a[kSymRW], b[kSymRW];
@@ -510,7 +517,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                     for (int q = 0; q < kSymRW; ++q) {
                         const int r = warp + q * kSymConsumers;
                         if (r < rows) {
-                            ypart[(int64_t)(row + r) * nb + J] = s[q];
+                            ypart[(int64_t)(row + r) * ldy + J] = s[q];
                             if (pdot) dacc = fma(sPI[r], s[q], dacc);
                         }
                     }
@@ -534,7 +541,9 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                 consumers_sync();
                 if (h == 0 && c < colsJ) {
                     const double colacc = part + colbuf[c];
-                    ypart[(int64_t)(J * kSymB + c) * nb + I] = colacc;
+                    // the tile's owner (holds strip 0) writes slot I; a head partial, its carry slot
+                    const int slot = (sa == 0) ? I : nb + rg.carry;
+                    ypart[(int64_t)(J * kSymB + c) * ldy + slot] = colacc;
                     if (pdot) dacc = fma(pj_c, colacc, dacc);
                 }
                 consumers_sync();
@@ -568,9 +577,54 @@ void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double
     const int nb = sym_ncb(P.n);
     const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(P.tmap_sym);
     if (mode == 1)
-        k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid, P.sym_keep);
+        k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, P.ncb, P.sym_ranges, dpart, sc,
+                                                             cid, P.sym_keep);
     else
-        k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, dpart, sc, cid, P.sym_keep);
+        k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, P.ncb, P.sym_ranges, dpart, sc,
+                                                             cid, P.sym_keep);
+}
+
+int sym_partition(int n, int grid, SymRange *out) {
+    const int nb = sym_ncb(n);
+    auto strips = [&](int I) { return (std::min(kSymB, n - I * kSymB) + kSymSR - 1) / kSymSR; };
+    int64_t total = 0;
+    for (int I = 0; I < nb; ++I) total += (int64_t)(nb - I) * strips(I);
+    // walk the tiles once, mapping each range boundary (a global strip index) to (tile, strip)
+    std::vector<int> tI, tJ;
+    std::vector<int64_t> tstart;
+    for (int I = 0; I < nb; ++I)
+        for (int J = I; J < nb; ++J) {
+            tstart.push_back(tstart.empty() ? 0 : tstart.back() + strips(tI.back()));
+            tI.push_back(I);
+            tJ.push_back(J);
+        }
+    const int ntiles = (int)tI.size();
+    auto locate = [&](int64_t g, int &t, int &s) {       // strip g -> (tile, strip), g <= total
+        if (g >= total) { t = ntiles; s = 0; return; }
+        int lo = 0, hi = ntiles - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (tstart[mid] <= g) lo = mid; else hi = mid - 1;
+        }
+        t = lo;
+        s = (int)(g - tstart[lo]);
+    };
+    std::vector<int> used(nb, 0);
+    int K = 0;
+    for (int b = 0; b < grid; ++b) {
+        SymRange r{};
+        const int64_t g0 = total * b / grid, g1 = total * (b + 1) / grid;
+        locate(g0, r.t0, r.s0);
+        locate(g1, r.t1, r.s1);
+        r.carry = -1;
+        if (g1 > g0 && r.s0 > 0 && tI[r.t0] != tJ[r.t0]) {
+            r.carry = used[tJ[r.t0]]++;
+            K = std::max(K, r.carry + 1);
+        }
+        if (g1 <= g0) { r.t0 = r.t1 = 0; r.s0 = r.s1 = 0; }   // empty range
+        if (out) out[b] = r;
+    }
+    return K;
 }
 
 // Exact-symmetry check at create (the symmetric GEMV is only used when H == H^T bitwise).
@@ -644,9 +698,9 @@ static int grid_for(int64_t units, int per_block) {
 }
 
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
-                 Scalars *sc, int mode, int check_done, cudaStream_t st) {
+                 Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid) {
     if (P.m == 0) return;
-    const int grid = grid_for(P.m, kBlock / 32);
+    const int grid = std::min(grid_for(P.m, kBlock / 32), max_grid);
     if (mode == 1)
         k_spmv<1><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV_PCG, check_done);
     else

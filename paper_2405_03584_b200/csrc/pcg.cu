@@ -329,6 +329,108 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
     }
 }
 
+// Fused update + next search direction (condensed, unsharded).  Same update as
+// k_pcg_update, then ONE grid barrier (cooperative launch: all CTAs co-resident); every CTA
+// sums the rz / rr partials in the same fixed order (bit-identical values everywhere), takes
+// the same stop decision, and — unless stopping — forms p = z + beta p and its S_b partial
+// for the rows it owns, so the next iteration needs no separate k_pcg_p launch.  The scalars
+// are read before the barrier and published by CTA 0 after it.
+template <int G>
+__global__ void __launch_bounds__(kBlock)
+k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
+                double *__restrict__ p, const double *__restrict__ pAt, double *__restrict__ x,
+                double *__restrict__ r, double *__restrict__ z, const double *__restrict__ Minv,
+                double *__restrict__ p1, double *__restrict__ p2, double *__restrict__ p3, Scalars *sc,
+                cudaGraphConditionalHandle h, int use_cond) {
+    __shared__ double red[kBlock / 32];
+    if (sc->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+        return;
+    }
+    const double pkp = sc->S_H + sc->S_b + sc->S_c;
+    if (!(pkp > 0.0) || !finite_d(pkp)) {           // uniform over the grid: nobody waits
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            fin_pcg_alpha(sc, pkp);
+            if (use_cond) cudaGraphSetConditional(h, 0);
+        }
+        return;
+    }
+    const double rho = sc->rho;
+    const double alpha = rho / pkp;
+    const int64_t it1 = sc->it + 1, maxit = sc->maxit;
+    const double tol2 = sc->tol2;
+    const int gl = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    double rz = 0.0, rr = 0.0;
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;
+        double pi = 0.0, sbi = 0.0, xi = 0.0, ri0 = 0.0, mi = 0.0, ati = 0.0;
+        if (gl == 0) {
+            pi = p[i];
+            sbi = sigb[i];
+            xi = x[i];
+            ri0 = r[i];
+            mi = Minv[i];
+            if (pAt != nullptr) ati = pAt[i];
+        }
+        double s = 0.0;
+        for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
+        s = group_sum<G>(s);
+        if (act && gl == 0) {
+            const double yi = fma(sbi, pi, s + ati);
+            x[i] = fma(alpha, pi, xi);
+            const double ri = fma(-alpha, yi, ri0);
+            r[i] = ri;
+            const double zi = mi * ri;
+            z[i] = zi;
+            rz = fma(ri, zi, rz);
+            rr = fma(ri, ri, rr);
+        }
+    }
+    const double a = block_sum(rz, red);
+    const double b = block_sum(rr, red);
+    if (threadIdx.x == 0) {
+        p1[blockIdx.x] = a;
+        p2[blockIdx.x] = b;
+    }
+    grid_barrier(&sc->counters[C_BAR], &sc->counters[C_BAR_GEN]);
+    const double trz = sum_partials(p1, gridDim.x, red);
+    const double trr = sum_partials(p2, gridDim.x, red);
+    int stop = (trr <= tol2 || it1 >= maxit) ? 1 : 0;
+    if (!finite_d(trr) || !finite_d(trz)) stop = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->pKp = pkp;
+        sc->alpha = alpha;
+        fin_pcg_update(sc, trz, trr);                  // rho_old, rho, rr, it, it_rs, done
+        if (use_cond) cudaGraphSetConditional(h, stop ? 0u : 1u);
+    }
+    if (stop) return;
+    const double beta = trz / rho;
+    // p and its S_b partials with exactly k_pcg_p's association (virtual blocks of kBlock
+    // threads over a grid of ceil(n / kBlock)), so the fused and unfused paths agree bitwise
+    const int gq = (n + kBlock - 1) / kBlock;
+    const int gp = gq < 1 ? 1 : (gq > kMaxGrid ? kMaxGrid : gq);
+    for (int vb = blockIdx.x; vb < gp; vb += gridDim.x) {
+        double acc = 0.0;
+        for (int i = vb * blockDim.x + threadIdx.x; i < n; i += gp * blockDim.x) {
+            const double pn = fma(beta, p[i], __ldcg(z + i));
+            p[i] = pn;
+            acc = fma(sigb[i] * pn, pn, acc);
+        }
+        const double c = block_sum(acc, red);
+        if (threadIdx.x == 0) p3[vb] = c;
+    }
+    if (last_block(&sc->counters[C_P2])) {
+        const double t = sum_partials(p3, gp, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_P2] = 0;
+            sc->S_b = t;
+            sc->loc[0] = t;
+        }
+    }
+}
+
 // ------------------------------------------------------------- tiny problems: one CTA
 // For n <= kSmallN the four-kernel iteration is launch-latency bound (C1: ~23 us per
 // iteration for ~1 us of work), so the whole PCG loop runs inside ONE 512-thread CTA:
@@ -447,9 +549,9 @@ k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, 
     }
 }
 
-static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st) {
+static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st, int max_grid = kMaxGrid) {
     if (P.m == 0 || P.n == 0) return;
-    const int g = grid_for(P.n, kBlock / G);
+    const int g = std::min(grid_for(P.n, kBlock / G), max_grid);
     switch (G) {
         case 4: k_spmvT<4><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
         case 8: k_spmvT<8><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
@@ -467,9 +569,7 @@ static int update_group(int ncb) {
         env = e ? atoi(e) : 0;
     }
     if (env == 4 || env == 8 || env == 16 || env == 32) return env;
-    if (ncb <= 16) return 4;
-    if (ncb <= 64) return 8;
-    return 16;
+    return ncb <= 40 ? 4 : 8;     // C3 (ncb 79+): 8 ~ 4 < 16 < 32 (scripts/pcg_iter_probe.py)
 }
 
 static void launch_update_g(const Prob &P, const Vecs &V, int /*G*/, int ncb, Scalars *sc, double *x,
@@ -490,6 +590,43 @@ static void launch_update_g(const Prob &P, const Vecs &V, int /*G*/, int ncb, Sc
 #undef IPM_UPD
 }
 
+// cooperative grid of the fused update: every CTA must be co-resident (grid barrier)
+template <int GG>
+static int fp_grid(int n) {
+    static int cap = 0;
+    if (!cap) {
+        int dev = 0, sms = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_update_fp<GG>, kBlock, 0);
+        cap = std::max(1, std::min(occ, 8)) * sms;
+    }
+    return std::min(grid_for(n, kBlock / GG), cap);
+}
+
+template <int GG>
+static void launch_update_fp_g(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x,
+                               cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
+    const double *pAt = (P.m > 0) ? V.pAt : nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(fp_grid<GG>(P.n));
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_pcg_update_fp<GG>, P.n, ncb, (const double *)V.ypart, (const double *)V.sig_b, V.pp,
+                       pAt, x, V.pr, V.pz, (const double *)V.Minv, V.part[5], V.part[6], V.part[2], sc, h, use_cond);
+}
+
+static void launch_update_fp(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x,
+                             cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
+    if (update_group(ncb) == 4) launch_update_fp_g<4>(P, V, ncb, sc, x, h, use_cond, st);
+    else launch_update_fp_g<8>(P, V, ncb, sc, x, h, use_cond, st);
+}
+
 // sharded path: t is complete (replicated on every rank) when this is called
 void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st) {
     launch_spmvT(P, V, G, sc, st);
@@ -498,32 +635,58 @@ void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc
 
 // the SpMV stage of an iteration: condensed t = sig_c o (A p), or (NEXT-2) the augmented
 // t = 2 sig_c o (A p_x) + p_l - p_u and the middle block rows y_l, y_u
-static void spmv_stage(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st) {
+static void spmv_stage(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st, int max_grid) {
     if (P.aug) launch_spmv_aug(P, V, V.pp, V.ag.pl, V.ag.pu, sc, 1, st);
-    else launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st);
-    launch_spmvT(P, V, G, sc, st);
+    else launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st, max_grid);
+    launch_spmvT(P, V, G, sc, st, max_grid);
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return sms;
+}
+
+// grid cap of the side-branch SpMV stage (IPM_SIDE_GRID overrides, experiments)
+static int side_grid() {
+    static int g = 0;
+    if (!g) {
+        const char *e = getenv("IPM_SIDE_GRID");
+        g = e ? atoi(e) : num_sms();
+        if (g < 1) g = kMaxGrid;
+    }
+    return g;
 }
 
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
-                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork) {
-    launch_pcg_p(P, V, sc, st);
-    if (!use_cond) dstage("pcg_p", st);
+                          cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, const Fork *fork, bool fused_p) {
+    // fused_p: p (and S_b) were formed by the previous iteration's k_pcg_update_fp, or by the
+    // k_pcg_p the caller launched after a (re)start
+    if (!fused_p) {
+        launch_pcg_p(P, V, sc, st);
+        if (!use_cond) dstage("pcg_p", st);
+    }
     // the SpMV stage only shares p with the GEMV: run it on a side stream (a parallel branch of
     // the captured graph) next to the HBM-bound GEMV; joined before the update.
     const bool par = fork != nullptr && P.m > 0;
     if (par) {
         cudaEventRecord(fork->ev_fork, st);
         cudaStreamWaitEvent(fork->side, fork->ev_fork, 0);
-        spmv_stage(P, V, G, sc, fork->side);
+        spmv_stage(P, V, G, sc, fork->side, side_grid());
         cudaEventRecord(fork->ev_join, fork->side);
     } else {
-        spmv_stage(P, V, G, sc, st);
+        spmv_stage(P, V, G, sc, st, kMaxGrid);
         if (!use_cond) dstage("spmv", st);
     }
     launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);
     if (!use_cond) dstage("gemv", st);
     if (par) cudaStreamWaitEvent(st, fork->ev_join, 0);
-    launch_update_g(P, V, G, ncb, sc, x, h, use_cond, st);
+    if (fused_p) launch_update_fp(P, V, ncb, sc, x, h, use_cond, st);
+    else launch_update_g(P, V, G, ncb, sc, x, h, use_cond, st);
 }
 
 }  // namespace ipm

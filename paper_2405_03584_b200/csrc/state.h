@@ -59,7 +59,7 @@ enum XStage { X_PCG_INIT = 0, X_PCG_ALPHA, X_PCG_UPDATE, X_PCG_RESTART, X_RES2, 
 enum Counter {
     C_GEMV = 0, C_GEMV_PCG, C_SPMV, C_SPMV_PCG, C_P, C_UPD, C_INIT_PCG, C_TRUE_RES, C_INIT_M, C_INIT_N,
     C_RES_M, C_RES_N, C_REC_M, C_REC_N, C_MUAFF_M, C_MUAFF_N, C_FINITE, C_LS_M, C_LS_N,
-    C_UPD2
+    C_UPD2, C_BAR, C_BAR_GEN, C_P2
 };
 
 // Read-only problem view.
@@ -83,6 +83,7 @@ struct Prob {
     int sym_keep;          // leading tiles of each CTA's range loaded with an L2 evict_last policy
     int ncb;               // column blocks of the ypart[row][cb] layout of the chosen GEMV
     const void *tmap_sym;  // host copy of the CUtensorMap over H (16 x 256 fp64 boxes)
+    const struct SymRange *sym_ranges;   // device: per-CTA strip ranges (kernels.h sym_partition)
     // compact quasi-Newton Hessian H = diag(h0) + U diag(w) U^T (compact.cu)
     int hess_compact;
     int ck;                // columns of U in use

@@ -60,8 +60,10 @@ class SQP:
             self.sqp_options = make_sqp_options(**sqp_options)
             self.qp_options = make_options(**(qp_options or {}))
             nb = C.c_size_t(0)
-            L.check(L.ipm_sqp_workspace_size(C.byref(cons), C.byref(nlp), C.byref(self.sqp_options),
-                                             C.byref(self.qp_options), C.byref(nb)), None)
+            st = L.ipm_sqp_workspace_size(C.byref(cons), C.byref(nlp), C.byref(self.sqp_options),
+                                          C.byref(self.qp_options), C.byref(nb))
+            if st != L.IPM_OK:
+                raise L.IpmError(st, (L.ipm_sqp_last_error(None) or b"").decode(errors="replace"))
             self.workspace = torch.empty(max(int(nb.value), 256), dtype=torch.uint8, device=dev)
             h = C.c_void_p()
             st = L.ipm_sqp_create(C.byref(h), C.byref(cons), C.byref(nlp), C.byref(self.sqp_options),

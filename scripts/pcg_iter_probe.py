@@ -21,6 +21,9 @@ qp.solve()
 res = {"workload": wl, "upd_g": os.environ.get("IPM_UPD_G"), "keep_mb": os.environ.get("IPM_SYM_KEEP_MB"),
        "persist_mb": os.environ.get("PERSIST_MB"), "gemv_ms": qp.profile("gemv", 30),
        "spmv_ms": qp.profile("spmv", 30) if q.m else None, "pcg_iter_ms": qp.profile("pcg_iter", 30)}
+if os.environ.get("PROBE_QP", "1") == "0":
+    print(json.dumps(res), flush=True)
+    sys.exit(0)
 qp2 = QP(device="cuda:0", **t)
 qp2.solve()
 ts = []

@@ -77,7 +77,8 @@ def test_gemv_kernels_agree_bitwise(n):
     assert np.linalg.norm(yb.cpu().numpy() - yref) <= 1e-12 * np.linalg.norm(yref)
 
 
-@pytest.mark.parametrize("n,m", [(1, 1), (255, 30), (256, 0), (1000, 200), (2049, 500), (5003, 300)])
+@pytest.mark.parametrize("n,m", [(1, 1), (255, 30), (256, 0), (300, 0), (700, 50), (1000, 200), (2049, 500),
+                                 (5003, 300), (12000, 0)])
 def test_symmetric_gemv_matches_oracle(n, m):
     """gemv_kernel=3 reads only the upper block triangle of the (exactly symmetric) H."""
     q = planted_qp(n, m, density=min(1.0, 0.02 + 2.0 / n), rank=min(48, n), seed=n + 3 * m,
