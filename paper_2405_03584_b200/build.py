@@ -25,10 +25,14 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
+    """variant "tl": diagnostic build with per-kernel timeline stamps (-DIPM_TIMELINE) into
+    libipm_tl.so; loaded only when IPM_LIB points at it (scripts/timeline_probe.py)."""
+    lib = LIB if not variant else LIB.replace("libipm.so", f"libipm_{variant}.so")
+    extra = ["-DIPM_TIMELINE"] if variant == "tl" else []
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers += [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     jobs = []
@@ -37,7 +41,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, *FLAGS, *extra, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -50,11 +54,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if verbose:
         for lg in logs:
             sys.stderr.write(lg)
-    if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fvisibility=hidden", "-ldl"]
+    if force or jobs or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-Xcompiler", "-fvisibility=hidden", "-ldl"]
         run(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, variant="tl" if "--timeline" in sys.argv else ""))

@@ -111,6 +111,14 @@ __device__ __forceinline__ void ktimer_stop(unsigned long long *neg, unsigned lo
     *cnt += 1;
 }
 
+#ifdef IPM_TIMELINE
+#define TL_BEGIN(sc, k) do { if (threadIdx.x == 0) atomicMax(&(sc)->tl[k][0], ~gtimer_ns()); } while (0)
+#define TL_END(sc, k) do { if (threadIdx.x == 0) atomicMax(&(sc)->tl[k][1], gtimer_ns()); } while (0)
+#else
+#define TL_BEGIN(sc, k) do { } while (0)
+#define TL_END(sc, k) do { } while (0)
+#endif
+
 // Grid-wide barrier for cooperatively launched kernels (all CTAs co-resident): arrival
 // counter + generation word.  The generation is read BEFORE arriving, so the last arrival's
 // increment cannot be missed; fences order every CTA's prior global writes before release.

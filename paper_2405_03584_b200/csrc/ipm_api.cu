@@ -928,6 +928,15 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             return fail(ctx, IPM_ERR_INVALID, "pcg_system = 1 (doubly augmented) is unsharded only");
         P.aug = (ctx->opt.pcg_system == 1 && p->m > 0) ? 1 : 0;
         ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
+        {
+            static bool carve = false;
+            const char *ce = getenv("IPM_CARVEOUT");
+            if (!carve && !(ce && atoi(ce) == 0)) {
+                configure_linalg_carveout();
+                configure_pcg_carveout();
+                carve = true;
+            }
+        }
         {   // fused update + p (cooperative grid barrier): single-GPU condensed PCG
             int coop = 0;
             CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
@@ -1200,6 +1209,15 @@ IPM_EXPORT ipm_status ipm_get_info(const ipm_ctx *ctx, ipm_info *info) {
 }
 
 IPM_EXPORT int64_t ipm_kernel_launches(const ipm_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+#ifdef IPM_TIMELINE
+// diagnostic builds only: the ring of per-iteration kernel timestamps (64 x 8 u64, ns)
+IPM_EXPORT ipm_status ipm_debug_timeline(ipm_ctx *ctx, unsigned long long *host) {
+    CK(cudaMemcpyAsync(host, ctx->sc->tl_ring, sizeof(ctx->sc->tl_ring), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return IPM_OK;
+}
+#endif
 
 IPM_EXPORT ipm_status ipm_kernel_timer(ipm_ctx *ctx, double *ms_total, int64_t *launches) {
     if (!ctx || !ms_total || !launches) return fail(ctx, IPM_ERR_INVALID, "bad argument");

@@ -47,11 +47,13 @@ bool make_sym_tensor_map(const Prob &P, void *out128);   // CUtensorMap (128 B, 
 int gemv_bulk_grid();
 void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb, double *dpart,
                       Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
-// max_grid: the PCG's side-branch launch caps the grid at one CTA per SM so the SpMV stage
-// co-resides with the one-CTA-per-SM symmetric GEMV instead of delaying its CTAs
+// max_grid: optional grid cap (the PCG side branch; see side_grid in pcg.cu)
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
-                 Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid = kMaxGrid);
+                 Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid = kMaxGrid,
+                 int block = kBlock);
 int num_sms();
+void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
+void configure_pcg_carveout();
 // NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,
 // yu = -A px + D_u pu (masked); mode 1 (PCG): done check + S_c = a.t + pl.yl + pu.yu
 void launch_spmv_aug(const Prob &P, const Vecs &V, const double *px, const double *pl, const double *pu, Scalars *sc,

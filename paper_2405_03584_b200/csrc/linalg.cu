@@ -407,6 +407,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
     __shared__ double colbuf[kSymB];                  // row-half-1 column sums of the current tile
     if (MODE == 1 && sc->done) return;
     if (MODE == 1) ktimer_start(&sc->kt_neg);
+    if (MODE == 1) TL_BEGIN(sc, 2);
     double *stages = reinterpret_cast<double *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kSymStages * kSymStageDoubles * 8);
     uint64_t *empty = full + kSymStages;
@@ -564,6 +565,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
             // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
     }
+    if (MODE == 1) TL_END(sc, 2);
 }
 
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
@@ -660,6 +662,7 @@ k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const
        double *__restrict__ dpart, Scalars *sc, int cid, int check_done) {
     __shared__ double red[kBlock / 32];
     if (check_done && sc->done) return;
+    if (MODE == 1) TL_BEGIN(sc, 0);
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     double dacc = 0.0;
@@ -688,6 +691,7 @@ k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const
             sc->S_c = tot;
         }
     }
+    TL_END(sc, 0);
 }
 
 static int grid_for(int64_t units, int per_block) {
@@ -698,11 +702,11 @@ static int grid_for(int64_t units, int per_block) {
 }
 
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
-                 Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid) {
+                 Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid, int block) {
     if (P.m == 0) return;
-    const int grid = std::min(grid_for(P.m, kBlock / 32), max_grid);
+    const int grid = std::min(grid_for(P.m, block / 32), max_grid);
     if (mode == 1)
-        k_spmv<1><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV_PCG, check_done);
+        k_spmv<1><<<grid, block, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV_PCG, check_done);
     else
         k_spmv<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV, check_done);
 }
@@ -1023,6 +1027,20 @@ __global__ void k_rank2(int nrows, int row0, int ncols, double *__restrict__ H, 
 void launch_rank2(const Prob &P, int row0, const double *u, double a, const double *v, double b, cudaStream_t st) {
     if (P.n == 0) return;
     k_rank2<<<kMaxGrid * 2, kBlock, 0, st>>>(P.n, row0, P.ncols, P.H, P.ldh, u, a, v, b, P.diagH);
+}
+
+// Kernels that run next to (or right after) the one-CTA-per-SM symmetric GEMV take the same
+// max-shared L1/smem carveout: otherwise an SM holding a GEMV CTA is not eligible for their
+// CTAs (different carveout) and the SpMV side branch waits for the GEMV to drain (measured:
+// the side branch started 215 us into a 240 us GEMV, scripts/timeline_probe.py).
+void configure_linalg_carveout() {
+    const int c = cudaSharedmemCarveoutMaxShared;
+    cudaFuncSetAttribute(k_spmv<0>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_spmv<1>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_spmv_aug<0>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_spmv_aug<1>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_symv_bulk<0>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
 }
 
 }  // namespace ipm

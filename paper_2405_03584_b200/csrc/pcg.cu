@@ -355,6 +355,7 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
         }
         return;
     }
+    TL_BEGIN(sc, 3);
     const double rho = sc->rho;
     const double alpha = rho / pkp;
     const int64_t it1 = sc->it + 1, maxit = sc->maxit;
@@ -400,6 +401,15 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
     int stop = (trr <= tol2 || it1 >= maxit) ? 1 : 0;
     if (!finite_d(trr) || !finite_d(trz)) stop = 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+#ifdef IPM_TIMELINE
+        unsigned long long *rec = sc->tl_ring[(it1 - 1) & 63];
+        for (int k = 0; k < 4; ++k) {
+            rec[2 * k] = ~sc->tl[k][0];
+            rec[2 * k + 1] = sc->tl[k][1];
+            sc->tl[k][0] = sc->tl[k][1] = 0ull;
+        }
+        rec[7] = gtimer_ns();                          // update: barrier passed
+#endif
         sc->pKp = pkp;
         sc->alpha = alpha;
         fin_pcg_update(sc, trz, trr);                  // rho_old, rho, rr, it, it_rs, done
@@ -533,8 +543,9 @@ void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
 template <int G>
 __global__ void __launch_bounds__(kBlock)
 k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, const double *__restrict__ ATval,
-        const double *__restrict__ t, double *__restrict__ out, const Scalars *sc) {
+        const double *__restrict__ t, double *__restrict__ out, Scalars *sc) {
     if (sc->done) return;
+    TL_BEGIN(sc, 1);
     const int gl = threadIdx.x & (G - 1);
     const int gpb = blockDim.x / G;
     // warp-uniform trip count: every lane reaches the group shuffles (full-mask __shfl_sync)
@@ -547,16 +558,18 @@ k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, 
         s = group_sum<G>(s);
         if (act && gl == 0) out[i] = s;
     }
+    TL_END(sc, 1);
 }
 
-static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st, int max_grid = kMaxGrid) {
+static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st, int max_grid = kMaxGrid,
+                         int block = kBlock) {
     if (P.m == 0 || P.n == 0) return;
-    const int g = std::min(grid_for(P.n, kBlock / G), max_grid);
+    const int g = std::min(grid_for(P.n, block / G), max_grid);
     switch (G) {
-        case 4: k_spmvT<4><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
-        case 8: k_spmvT<8><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
-        case 16: k_spmvT<16><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
-        default: k_spmvT<32><<<g, kBlock, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        case 4: k_spmvT<4><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        case 8: k_spmvT<8><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        case 16: k_spmvT<16><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        default: k_spmvT<32><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
     }
 }
 
@@ -635,10 +648,10 @@ void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc
 
 // the SpMV stage of an iteration: condensed t = sig_c o (A p), or (NEXT-2) the augmented
 // t = 2 sig_c o (A p_x) + p_l - p_u and the middle block rows y_l, y_u
-static void spmv_stage(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st, int max_grid) {
+static void spmv_stage(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st, int max_grid, int block) {
     if (P.aug) launch_spmv_aug(P, V, V.pp, V.ag.pl, V.ag.pu, sc, 1, st);
-    else launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st, max_grid);
-    launch_spmvT(P, V, G, sc, st, max_grid);
+    else launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], sc, 1, 1, st, max_grid, block);
+    launch_spmvT(P, V, G, sc, st, max_grid, block);
 }
 
 int num_sms() {
@@ -651,15 +664,32 @@ int num_sms() {
     return sms;
 }
 
-// grid cap of the side-branch SpMV stage (IPM_SIDE_GRID overrides, experiments)
+// grid cap of the side-branch SpMV stage (IPM_SIDE_GRID overrides, experiments).  Measured
+// at C3: capping it at one CTA per SM (148) or fewer makes the SpMV stage the critical path
+// (PCG iteration 0.275 ms at 1184 CTAs, 0.297 at 296, 0.331 at 148), so the full grid stays.
 static int side_grid() {
     static int g = 0;
     if (!g) {
         const char *e = getenv("IPM_SIDE_GRID");
-        g = e ? atoi(e) : num_sms();
+        g = e ? atoi(e) : kMaxGrid;
         if (g < 1) g = kMaxGrid;
     }
     return g;
+}
+
+// CTA size of the side-branch SpMV stage.  The symmetric GEMV CTA (17 warps x 96 registers)
+// leaves 1024 registers free on one SM sub-partition (warps are dealt round-robin to the four
+// SMSPs), so a 256-thread CTA (two 32-register warps per SMSP) cannot co-reside with it and the
+// SpMV stage waited for the GEMV to drain (timeline_probe: SpMV start 211 us into a 238 us
+// GEMV); 128-thread CTAs (one warp per SMSP) fit next to it.  IPM_SIDE_BLOCK overrides.
+static int side_block() {
+    static int b = 0;
+    if (!b) {
+        const char *e = getenv("IPM_SIDE_BLOCK");
+        b = e ? atoi(e) : 128;
+        if (b != 32 && b != 64 && b != 128 && b != 256) b = 128;
+    }
+    return b;
 }
 
 void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv_grid, Scalars *sc, double *x,
@@ -676,10 +706,10 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
     if (par) {
         cudaEventRecord(fork->ev_fork, st);
         cudaStreamWaitEvent(fork->side, fork->ev_fork, 0);
-        spmv_stage(P, V, G, sc, fork->side, side_grid());
+        spmv_stage(P, V, G, sc, fork->side, side_grid(), side_block());
         cudaEventRecord(fork->ev_join, fork->side);
     } else {
-        spmv_stage(P, V, G, sc, st, kMaxGrid);
+        spmv_stage(P, V, G, sc, st, kMaxGrid, kBlock);
         if (!use_cond) dstage("spmv", st);
     }
     launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);
@@ -687,6 +717,22 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
     if (par) cudaStreamWaitEvent(st, fork->ev_join, 0);
     if (fused_p) launch_update_fp(P, V, ncb, sc, x, h, use_cond, st);
     else launch_update_g(P, V, G, ncb, sc, x, h, use_cond, st);
+}
+
+// same carveout as the symmetric GEMV for the PCG-loop kernels (see linalg.cu)
+void configure_pcg_carveout() {
+    const int c = cudaSharedmemCarveoutMaxShared;
+    cudaFuncSetAttribute(k_spmvT<4>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_spmvT<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_spmvT<16>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_spmvT<32>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<4>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update<4>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update<16>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update<32>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_p, cudaFuncAttributePreferredSharedMemoryCarveout, c);
 }
 
 }  // namespace ipm

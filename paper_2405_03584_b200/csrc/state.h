@@ -51,6 +51,12 @@ struct Scalars {
     // kt_neg = max over CTAs of ~(start %globaltimer) (so 0 = unset), reset by the last CTA,
     // which adds (its end - earliest start) to kt_ns and counts the launch.
     unsigned long long kt_neg, kt_ns, kt_count;
+#ifdef IPM_TIMELINE
+    // diagnostic builds only (scripts/timeline_probe.py): per-kernel first-CTA start (as ~t)
+    // and last thread-0 exit of the current PCG iteration, copied into a ring by the update
+    unsigned long long tl[4][2];
+    unsigned long long tl_ring[64][8];
+#endif
 };
 
 // Combine stages of k_xcombine (shard.cu).
