@@ -304,7 +304,7 @@ ipm_status pcg_iteration_sharded(ipm_ctx *ctx) {
     launch_pcg_p(P, V, ctx->sc, ctx->st);
     const double *pf = nullptr;
     TRY(gather(ctx, V.pp, &pf));
-    launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
+    launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st, kMaxGrid, side_block());
     launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, ctx->st);
     TRY(xcombine(ctx, X_PCG_ALPHA));
     launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, ctx->st);

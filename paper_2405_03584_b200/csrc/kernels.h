@@ -52,6 +52,7 @@ void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, 
                  Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid = kMaxGrid,
                  int block = kBlock);
 int num_sms();
+int side_block();   // CTA size of every PCG-mode SpMV launch (one association => bitwise paths)
 void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
 void configure_pcg_carveout();
 // NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,

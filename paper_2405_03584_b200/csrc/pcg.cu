@@ -682,7 +682,7 @@ static int side_grid() {
 // SMSPs), so a 256-thread CTA (two 32-register warps per SMSP) cannot co-reside with it and the
 // SpMV stage waited for the GEMV to drain (timeline_probe: SpMV start 211 us into a 238 us
 // GEMV); 128-thread CTAs (one warp per SMSP) fit next to it.  IPM_SIDE_BLOCK overrides.
-static int side_block() {
+int side_block() {
     static int b = 0;
     if (!b) {
         const char *e = getenv("IPM_SIDE_BLOCK");
@@ -709,7 +709,7 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
         spmv_stage(P, V, G, sc, fork->side, side_grid(), side_block());
         cudaEventRecord(fork->ev_join, fork->side);
     } else {
-        spmv_stage(P, V, G, sc, st, kMaxGrid, kBlock);
+        spmv_stage(P, V, G, sc, st, kMaxGrid, side_block());   // same association as the side branch
         if (!use_cond) dstage("spmv", st);
     }
     launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);

@@ -45,10 +45,10 @@ for gk in [int(a) for a in sys.argv[1:]] or [3, 2]:
     gemv = qp.profile("gemv", 5)
     it = qp.profile("pcg_iter", 5)
     info = qp.info()
-    ncb = info["ncb"]
     if info["gemv_kernel"] == 3:
-        sizes = [min(256, n - i * 256) for i in range(ncb)]
-        streamed = 8.0 * sum(sizes[i] * sizes[j] for i in range(ncb) for j in range(i, ncb))
+        nb = (n + 255) // 256          # info["ncb"] also counts the carry slots
+        sizes = [min(256, n - i * 256) for i in range(nb)]
+        streamed = 8.0 * sum(sizes[i] * sizes[j] for i in range(nb) for j in range(i, nb))
     else:
         streamed = 8.0 * n * n
     print(json.dumps({"workload": "C5", "gemv_kernel": info["gemv_kernel"], "sampled_rel_err": err,

@@ -6,6 +6,8 @@
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o stream_bw stream_bw.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
+#include <algorithm>
 #include <cuda_runtime.h>
 
 __global__ void k_full(const double2 *__restrict__ a, int64_t n2, double *out) {
@@ -22,7 +24,7 @@ __global__ void k_full(const double2 *__restrict__ a, int64_t n2, double *out) {
     if (s == 1.2345) out[0] = s;
 }
 
-template <int ROWS>
+template <int ROWS, int TB = 256>
 __global__ void k_tri(const double *__restrict__ H, int n, int nb, double *out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int64_t nt = (int64_t)nb * (nb + 1) / 2;
@@ -35,15 +37,16 @@ __global__ void k_tri(const double *__restrict__ H, int n, int nb, double *out) 
     }
     double s = 0.0;
     for (int64_t t = t0; t < t1; ++t) {
-        const int r0 = I * 256, c0 = J * 256;
-        const int rows = min(256, n - r0), cols = min(256, n - c0);
+        const int r0 = I * TB, c0 = J * TB;
+        const int rows = min(TB, n - r0), cols = min(TB, n - c0);
+        constexpr int KV = TB / 64;                 // 16-B loads per lane per row
         for (int r = warp * ROWS; r < rows; r += nw * ROWS) {
-            double2 v[ROWS][4];
+            double2 v[ROWS][KV];
 #pragma unroll
             for (int q = 0; q < ROWS; ++q) {
                 const double2 *row = reinterpret_cast<const double2 *>(H + (int64_t)(r0 + r + q) * n + c0);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < KV; ++k) {
                     const int col = 2 * (lane + 32 * k);
                     v[q][k] = (r + q < rows && col < cols) ? __ldcs(row + lane + 32 * k) : make_double2(0, 0);
                 }
@@ -51,15 +54,15 @@ __global__ void k_tri(const double *__restrict__ H, int n, int nb, double *out) 
 #pragma unroll
             for (int q = 0; q < ROWS; ++q)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s += v[q][k].x * v[q][k].y;
+                for (int k = 0; k < KV; ++k) s += v[q][k].x * v[q][k].y;
         }
         if (++J == nb) { ++I; J = I; }
     }
     if (s == 1.2345) out[0] = s;
 }
 
-int main() {
-    const int n = 20000;
+int main(int argc, char **argv) {
+    const int n = argc > 1 ? atoi(argv[1]) : 20000;
     double *H, *out;
     cudaMalloc(&H, (size_t)n * n * 8);
     cudaMalloc(&out, 8);
@@ -69,9 +72,10 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const int nb = (n + 255) / 256;
-    double tri = 0;
+    const int nb = (n + 255) / 256, nb2 = (n + 511) / 512;
+    double tri = 0, tri2 = 0;
     for (int i = 0; i < nb; ++i) for (int j = i; j < nb; ++j) tri += (double)std::min(256, n - i * 256) * std::min(256, n - j * 256);
+    for (int i = 0; i < nb2; ++i) for (int j = i; j < nb2; ++j) tri2 += (double)std::min(512, n - i * 512) * std::min(512, n - j * 512);
     auto run = [&](const char *name, double bytes, auto launch) {
         for (int w = 0; w < 3; ++w) launch();
         cudaEventRecord(e0);
@@ -89,8 +93,16 @@ int main() {
             snprintf(nm, 64, "full cps=%d thr=%d", cps, thr);
             run(nm, (double)n * n * 8, [&] { k_full<<<sms * cps, thr>>>((const double2 *)H, (int64_t)n * n / 2, out); });
         }
-    for (int cps : {1, 2, 3, 4})
-        for (int thr : {256, 512, 1024}) {
+    for (int cps : {1, 2})
+        for (int thr : {512, 1024}) {
+            char nm[64];
+            snprintf(nm, 64, "tri512 R2 cps=%d thr=%d", cps, thr);
+            run(nm, tri2 * 8, [&] { k_tri<2, 512><<<sms * cps, thr>>>(H, n, nb2, out); });
+            snprintf(nm, 64, "tri512 R4 cps=%d thr=%d", cps, thr);
+            run(nm, tri2 * 8, [&] { k_tri<4, 512><<<sms * cps, thr>>>(H, n, nb2, out); });
+        }
+    for (int cps : {1, 2, 4})
+        for (int thr : {512, 1024}) {
             char nm[64];
             snprintf(nm, 64, "tri R2 cps=%d thr=%d", cps, thr);
             run(nm, tri * 8, [&] { k_tri<2><<<sms * cps, thr>>>(H, n, nb, out); });
