@@ -237,6 +237,16 @@ ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const
  *   what = 2: one full PCG iteration (all four kernels).  Clobbers PCG scratch state. */
 ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, double *ms_host);
 
+/* Host-only test hook (no device work): the work plan of the symmetric GEMV for global size
+ * ncols split over nranks (equal chunks, rank's view) and `grid` CTAs.  Tiles are reported as
+ * 8 int32 each {r0 (local), rows, c0 (global), cols, rslot, cmode, cbase, cslot}, ranges as 5
+ * int32 per CTA {t0, s0, t1, s1, carry}; NULL outputs are skipped, at most cap tiles are
+ * copied, *ntiles is always the full count.  *ldy / *ldz: ypart / remote-part strides.
+ * Every ordered entry (i, j) of H must be used exactly once across ranks (tests/test_abi.py). */
+ipm_status ipm_sym_plan(int32_t ncols, int32_t nranks, int32_t rank, int32_t grid, int32_t *tiles_host,
+                        int32_t cap, int32_t *ntiles_host, int32_t *ranges_host, int32_t *ldy_host,
+                        int32_t *ldz_host);
+
 /* Number of kernel launches the library issued since create (graph nodes count once per
  * executed node); used by bench.py's gpu_launches. */
 int64_t ipm_kernel_launches(const ipm_ctx *ctx);

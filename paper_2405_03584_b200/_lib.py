@@ -115,6 +115,8 @@ _sigs = {
     "ipm_profile": ([_P, C.c_int32, C.c_int32, C.POINTER(_D)], _S),
     "ipm_kernel_launches": ([_P], C.c_int64),
     "ipm_kernel_timer": ([_P, C.POINTER(_D), C.POINTER(C.c_int64)], _S),
+    "ipm_sym_plan": ([C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.POINTER(C.c_int32), _P,
+                      C.POINTER(C.c_int32), C.POINTER(C.c_int32)], _S),
     "ipm_last_error": ([_P], C.c_char_p),
     "ipm_destroy": ([_P], None),
     "ipm_sqp_options_default": ([C.POINTER(ipm_sqp_options)], None),

@@ -122,17 +122,24 @@ __device__ __forceinline__ void ktimer_stop(unsigned long long *neg, unsigned lo
 // Grid-wide barrier for cooperatively launched kernels (all CTAs co-resident): arrival
 // counter + generation word.  The generation is read BEFORE arriving, so the last arrival's
 // increment cannot be missed; fences order every CTA's prior global writes before release.
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned int g = *(volatile unsigned int *)gen;
+        const unsigned int g = ld_acquire_u32(gen);
         __threadfence();
         if (atomicAdd(count, 1u) == gridDim.x - 1) {
             *(volatile unsigned int *)count = 0u;
             __threadfence();
             atomicAdd(gen, 1u);
         } else {
-            while (*(volatile unsigned int *)gen == g) __nanosleep(20);
+            while (ld_acquire_u32(gen) == g) {
+            }
         }
         __threadfence();
     }

@@ -74,7 +74,7 @@ struct Offsets {
     size_t nvec[40];
     size_t mvec[40];
     size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad, gfull, xloc_all;
-    size_t ch0, cw, cs, cspart, chpart, symr;
+    size_t ch0, cw, cs, cspart, chpart, symr, symt, symz, zcol, zvec, zall, hashes;
     int n_nvec, n_mvec;
     int nchunk;
 };
@@ -84,8 +84,11 @@ constexpr int kMVec = 38;   // m-space vectors (24 + 14 segments of the doubly a
 
 // nloc = rows owned by this rank; every n-space vector gets chunk = ceil(n/P) (+2 pad) slots
 // so the allgather can send equal blocks and the bulk GEMV may read one padding element.
-Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks, Layout &L, int64_t ldu = 0) {
+Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks, Layout &L, int64_t ldu = 0,
+             int rank = 0, SymPlan *symp = nullptr) {
     Offsets o{};
+    SymPlan sp;
+    sym_plan_build((int)ncols, nranks, rank, gemv_bulk_grid(), sp);
     if (ldu > 0) {                     // compact Hessian (NEXT-1): h0, w, s = U^T p and partials
         o.ch0 = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
         o.cw = L.take(sizeof(double) * ldu);
@@ -97,10 +100,15 @@ Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks
     o.sc = L.take(sizeof(Scalars));
     for (int i = 0; i < kNVec; ++i) o.nvec[i] = L.take(sizeof(double) * (std::max<int64_t>(chunk, 1) + 2));
     for (int i = 0; i < kMVec; ++i) o.mvec[i] = L.take(sizeof(double) * std::max<int64_t>(m, 1));
-    const int symK = (nranks == 1) ? sym_partition((int)ncols, gemv_bulk_grid(), nullptr) : 0;
-    o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) *
-                     std::max(gemv_ncb((int)ncols), sym_ncb((int)ncols) + symK));
-    o.symr = L.take(sizeof(SymRange) * (size_t)gemv_bulk_grid());
+    o.ypart = L.take(sizeof(double) * std::max<int64_t>(nloc, 1) * std::max(gemv_ncb((int)ncols), sp.ldy));
+    o.symr = L.take(sizeof(SymRange) * sp.ranges.size());
+    o.symt = L.take(sizeof(SymTile) * std::max<size_t>(1, sp.tiles.size()));
+    o.symz = L.take(sizeof(double) * std::max<int64_t>(1, (int64_t)sp.zrows * sp.ldz));
+    o.zcol = L.take(sizeof(int) * std::max<size_t>(1, sp.zcol.size()));
+    o.zvec = L.take(sizeof(double) * (nranks > 1 ? ncols : 1));
+    o.zall = L.take(sizeof(double) * (nranks > 1 ? ncols * nranks : 1));
+    o.hashes = L.take(sizeof(unsigned long long) * (size_t)(nranks + 1) * (nranks + 1));
+    if (symp) *symp = std::move(sp);
     o.part = L.take(sizeof(double) * kMaxPartials * 8);
     o.ATrp = L.take(sizeof(int64_t) * (nloc + 1));
     o.ATcol = L.take(sizeof(int) * std::max<int64_t>(nnz_loc, 1));
@@ -143,6 +151,10 @@ struct ipm_ctx {
     cudaGraphConditionalHandle handle = 0;
     bool graph_ready = false;
     bool fused_p = false;        // PCG iterations use k_pcg_update_fp (p-update fused, cooperative)
+    bool sym_sharded = false;    // row-sharded symmetric GEMV: remote column parts exchanged per apply
+    int sym_zrows = 0;
+    int *sym_zcol = nullptr;
+    double *sym_zvec = nullptr, *sym_zall = nullptr;
     // state
     bool have_iterate = false;   // V holds a valid iterate (after a solve or set_iterate)
     bool user_iterate = false;   // set_iterate called: next solve starts from it
@@ -247,6 +259,23 @@ ipm_status gather(ipm_ctx *ctx, const double *local, const double **full) {
     return IPM_OK;
 }
 
+// Sharded symmetric GEMV: the column parts this rank computed for other ranks' rows (zpart)
+// are reduced to a full-length vector, allgathered, and each rank adds the P contributions to
+// its rows in rank order into the last ypart slot (shard.cu).  No-op otherwise.
+ipm_status sym_exchange(ipm_ctx *ctx) {
+    if (!ctx->sym_sharded) return IPM_OK;
+    const Prob &P = ctx->P;
+    launch_zreduce(ctx->sym_zrows, P.sym_ldz, P.sym_z, ctx->sym_zcol, ctx->sym_zvec, ctx->st);
+    CKL();
+    std::string e;
+    if (ctx->comm->allgather(ctx->sym_zvec, ctx->sym_zall, sizeof(double) * P.ncols, ctx->st, e))
+        return fail(ctx, IPM_ERR_NCCL, "%s", e.c_str());
+    launch_zfold(P.n, P.ncols, ctx->comm->nranks, ctx->row0, ctx->sym_zall, ctx->V.ypart, ctx->ncb, ctx->st);
+    ctx->launches += 2;
+    CKL();
+    return IPM_OK;
+}
+
 // Combine this stage's per-rank partials (Scalars::loc) across ranks (shard.cu).
 ipm_status xcombine(ipm_ctx *ctx, int stage, double p0 = 0.0, double p1 = 0.0, int64_t p2 = 0) {
     if (!ctx->sharded) return IPM_OK;
@@ -289,6 +318,7 @@ ipm_status op_apply(ipm_ctx *ctx, const double *v_local, const double *v_full, d
     if (aug) launch_spmv_aug(P, V, v_full, V.ag.xl, V.ag.xu, ctx->sc, 0, ctx->st);
     else launch_spmv(P, v_full, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 0, ctx->st);
     launch_gemv(P, v_full, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+    TRY(sym_exchange(ctx));
     launch_apply_reduce(P, ctx->G, ctx->ncb, V.ypart, V.sig_b, v_local, V.pt, out, rhs, V.part[5], ctx->sc, mode,
                         ctx->st, aug ? &ag : nullptr);
     ctx->launches += (P.m > 0 ? 1 : 0) + 2;
@@ -306,6 +336,7 @@ ipm_status pcg_iteration_sharded(ipm_ctx *ctx) {
     TRY(gather(ctx, V.pp, &pf));
     launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st, kMaxGrid, side_block());
     launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, ctx->st);
+    TRY(sym_exchange(ctx));
     TRY(xcombine(ctx, X_PCG_ALPHA));
     launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, ctx->st);
     TRY(xcombine(ctx, X_PCG_UPDATE));
@@ -327,8 +358,13 @@ ipm_status build_graph(ipm_ctx *ctx) {
     CK(cudaGraphAddNode(&node, ctx->graph, nullptr, 0, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(ctx->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle, 1, ctx->cap,
-                         &ctx->fork, ctx->fused_p);
+    // IPM_UNROLL (experiment): k PCG iterations per WHILE trip; an iteration after the stop
+    // early-exits in every kernel (sc->done), and the last update sets the condition
+    const char *ue = getenv("IPM_UNROLL");
+    const int unroll = ue ? std::max(1, std::min(8, atoi(ue))) : 1;
+    for (int u = 0; u < unroll; ++u)
+        launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle, 1,
+                             ctx->cap, &ctx->fork, ctx->fused_p);
     cudaGraph_t captured = nullptr;
     CK(cudaStreamEndCapture(ctx->cap, &captured));
     CK(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
@@ -440,6 +476,7 @@ ipm_status residuals(ipm_ctx *ctx, double mu) {
     const double *xf = nullptr;
     TRY(gather(ctx, V.x, &xf));
     launch_gemv(P, xf, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+    TRY(sym_exchange(ctx));
     DSYNC("gemv Hx");
     launch_spmv(P, xf, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
     DSYNC("spmv Ax");
@@ -713,7 +750,7 @@ IPM_EXPORT ipm_status ipm_workspace_size(const ipm_problem *p, const ipm_options
     Layout L;
     if (p->hess_kind == 1 && (p->ldu < 1 || p->k < 0 || p->k > p->ldu))
         return fail(nullptr, IPM_ERR_INVALID, "compact Hessian needs 0 <= k <= ldu and ldu >= 1");
-    plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L, p->hess_kind == 1 ? p->ldu : 0);   // local A^T nnz <= nnz
+    plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L, p->hess_kind == 1 ? p->ldu : 0, p->rank);   // local A^T nnz <= nnz
     *bytes = L.total;
     return IPM_OK;
 }
@@ -790,7 +827,9 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
 
         // --- device state ------------------------------------------------------------
         Layout L;
-        const Offsets o = plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L, p->hess_kind == 1 ? p->ldu : 0);
+        SymPlan symp;
+        const Offsets o = plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L, p->hess_kind == 1 ? p->ldu : 0,
+                               eff_ranks(p) > 1 ? p->rank : 0, &symp);
         CK(cudaMemsetAsync(ctx->ws, 0, L.total, ctx->st));
         ctx->sc = reinterpret_cast<Scalars *>(ctx->ws + o.sc);
         assign_vectors(ctx, o);
@@ -880,23 +919,54 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         const int gk = ctx->opt.gemv_kernel;
         const bool bulk_ok = gemv_bulk_ok(P);
         bool sym = false;
-        if ((gk == 0 || gk == 3) && !ctx->sharded && bulk_ok && !P.hess_compact) {
-            // the symmetric GEMV reads only H's upper block triangle: require H == H^T bitwise
-            unsigned long long nasym = 0;
-            CK(cudaMemsetAsync(bad, 0, sizeof nasym, ctx->st));
-            launch_count_asym(P, bad, ctx->st);
-            CKL();
-            CK(cudaMemcpyAsync(&nasym, bad, sizeof nasym, cudaMemcpyDeviceToHost, ctx->st));
-            CK(cudaStreamSynchronize(ctx->st));
+        P.row_begin = ctx->row0;
+        const bool sym_try = (gk == 0 || gk == 3) && !P.hess_compact && (!ctx->sharded || (ctx->chunk % 2) == 0);
+        if (sym_try) {
+            // the symmetric GEMV reads only an upper block triangle: require H == H^T bitwise.
+            // Unsharded: every entry pair compared.  Sharded: the rank's diagonal block compared
+            // entry by entry, the off-diagonal blocks certified by exchanged order-independent
+            // hashes (k_sym_hash) — every rank takes the same decision from the same data.
+            unsigned long long nasym = bulk_ok ? 0ull : 1ull;
+            if (bulk_ok) {
+                Prob Q = P;
+                Q.H = P.H + (ctx->sharded ? ctx->row0 : 0);      // the local diagonal block
+                CK(cudaMemsetAsync(bad, 0, sizeof nasym, ctx->st));
+                launch_count_asym(Q, bad, ctx->st);
+                CKL();
+                CK(cudaMemcpyAsync(&nasym, bad, sizeof nasym, cudaMemcpyDeviceToHost, ctx->st));
+                CK(cudaStreamSynchronize(ctx->st));
+                ctx->launches += 1;
+            }
             sym = (nasym == 0);
-            ctx->launches += 1;
+            if (ctx->sharded) {
+                const int R = ctx->comm->nranks;
+                unsigned long long *hs = reinterpret_cast<unsigned long long *>(ctx->ws + o.hashes);
+                CK(cudaMemsetAsync(hs, 0, sizeof(unsigned long long) * (R + 1), ctx->st));
+                if (bulk_ok) launch_sym_hash(P.n, P.ncols, ctx->row0, (int)ctx->chunk, R, P.H, P.ldh, hs, ctx->st);
+                CK(cudaMemcpyAsync(hs + R, &nasym, sizeof nasym, cudaMemcpyHostToDevice, ctx->st));
+                std::string e;
+                if (ctx->comm->allgather(hs, hs + (R + 1), sizeof(unsigned long long) * (R + 1), ctx->st, e))
+                    return fail(ctx, IPM_ERR_NCCL, "%s", e.c_str());
+                std::vector<unsigned long long> all((size_t)R * (R + 1));
+                CK(cudaMemcpyAsync(all.data(), hs + (R + 1), sizeof(unsigned long long) * all.size(),
+                                   cudaMemcpyDeviceToHost, ctx->st));
+                CK(cudaStreamSynchronize(ctx->st));
+                ctx->launches += 1;
+                sym = true;
+                for (int a = 0; a < R; ++a) {
+                    if (all[(size_t)a * (R + 1) + R] != 0) sym = false;
+                    for (int b = 0; b < R; ++b)
+                        if (a != b && all[(size_t)a * (R + 1) + b] != all[(size_t)b * (R + 1) + a]) sym = false;
+                }
+            }
             if (sym) {
                 sym = make_sym_tensor_map(P, ctx->tmap_sym);
                 P.tmap_sym = ctx->tmap_sym;
             }
         }
         if (gk == 3 && !sym)
-            return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=3 needs an unsharded, exactly symmetric H with even ldh");
+            return fail(ctx, IPM_ERR_INVALID,
+                        "gemv_kernel=3 needs an exactly symmetric H, even ldh, 16-byte aligned rows (sharded: even chunk)");
         if (gk == 2 && !bulk_ok) return fail(ctx, IPM_ERR_INVALID, "gemv_kernel=2 needs even ldh and 16-byte aligned H");
         P.gemv_sym = sym ? 1 : 0;
         P.sym_keep = 0;
@@ -912,16 +982,31 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         }
         P.gemv_bulk = (!sym && !P.hess_compact && (gk == 0 || gk == 2) && bulk_ok) ? 1 : 0;
         P.gemv_bulk_grid = gemv_bulk_grid();
-        int symK = 0;
-        if (sym) {                  // strip-balanced ranges of the symmetric GEMV (kernels.h)
-            std::vector<SymRange> rg((size_t)P.gemv_bulk_grid);
-            symK = sym_partition((int)p->n, P.gemv_bulk_grid, rg.data());
-            SymRange *d = reinterpret_cast<SymRange *>(ctx->ws + o.symr);
-            CK(cudaMemcpyAsync(d, rg.data(), sizeof(SymRange) * rg.size(), cudaMemcpyHostToDevice, ctx->st));
+        if (sym) {                  // the SYMV work plan (tiles, strip-balanced ranges; kernels.h)
+            SymTile *dt = reinterpret_cast<SymTile *>(ctx->ws + o.symt);
+            SymRange *dr = reinterpret_cast<SymRange *>(ctx->ws + o.symr);
+            int *dz = reinterpret_cast<int *>(ctx->ws + o.zcol);
+            CK(cudaMemcpyAsync(dt, symp.tiles.data(), sizeof(SymTile) * symp.tiles.size(), cudaMemcpyHostToDevice,
+                               ctx->st));
+            CK(cudaMemcpyAsync(dr, symp.ranges.data(), sizeof(SymRange) * symp.ranges.size(),
+                               cudaMemcpyHostToDevice, ctx->st));
+            if (!symp.zcol.empty())
+                CK(cudaMemcpyAsync(dz, symp.zcol.data(), sizeof(int) * symp.zcol.size(), cudaMemcpyHostToDevice,
+                                   ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
-            P.sym_ranges = d;
+            P.sym_tiles = dt;
+            P.sym_ranges = dr;
+            P.sym_z = reinterpret_cast<double *>(ctx->ws + o.symz);
+            P.sym_ycarry = symp.nbg;
+            P.sym_ldz = symp.ldz;
+            P.sym_zcarry = symp.ldz - symp.zcarry_n;
+            ctx->sym_zrows = symp.zrows;
+            ctx->sym_zcol = dz;
+            ctx->sym_zvec = reinterpret_cast<double *>(ctx->ws + o.zvec);
+            ctx->sym_zall = reinterpret_cast<double *>(ctx->ws + o.zall);
+            ctx->sym_sharded = ctx->sharded;
         }
-        ctx->ncb = P.hess_compact ? 1 : (sym ? sym_ncb((int)p->n) + symK : gemv_ncb((int)p->n));
+        ctx->ncb = P.hess_compact ? 1 : (sym ? symp.ldy : gemv_ncb((int)p->n));
         P.ncb = ctx->ncb;
         if (ctx->opt.pcg_system != 0 && ctx->opt.pcg_system != 1) return fail(ctx, IPM_ERR_INVALID, "unknown pcg_system");
         if (ctx->opt.pcg_system == 1 && ctx->sharded)
@@ -1173,7 +1258,9 @@ IPM_EXPORT ipm_status ipm_profile(ipm_ctx *ctx, int32_t what, int32_t reps, doub
     if (what == 2 && ctx->fused_p) launch_pcg_p(P, V, ctx->sc, ctx->st);
     auto one = [&]() {
         // what 0: the PCG GEMV's full work (tiles + fused p^T H p) without its done/alpha epilogue
-        if (what == 0) launch_gemv(P, V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV_PCG, ctx->st);
+        // (sharded: the GEMV reads a full-length vector — the last allgathered one)
+        if (what == 0) launch_gemv(P, ctx->sharded ? V.gfull : V.pp, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc,
+                                   ctx->gemv_grid, 0, C_GEMV_PCG, ctx->st);
         else if (what == 1 && P.aug) launch_spmv_aug(P, V, V.pp, V.ag.pl, V.ag.pu, ctx->sc, 1, ctx->st);
         else if (what == 1) launch_spmv(P, V.pp, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st);
         else launch_pcg_iteration(P, V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, V.dx, 0, 0, ctx->st, &ctx->fork,
@@ -1209,6 +1296,30 @@ IPM_EXPORT ipm_status ipm_get_info(const ipm_ctx *ctx, ipm_info *info) {
 }
 
 IPM_EXPORT int64_t ipm_kernel_launches(const ipm_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+IPM_EXPORT ipm_status ipm_sym_plan(int32_t ncols, int32_t nranks, int32_t rank, int32_t grid, int32_t *tiles,
+                                   int32_t cap, int32_t *ntiles, int32_t *ranges, int32_t *ldy, int32_t *ldz) {
+    if (ncols < 1 || nranks < 1 || rank < 0 || rank >= nranks || grid < 1 || !ntiles)
+        return fail(nullptr, IPM_ERR_INVALID, "bad argument");
+    SymPlan pl;
+    sym_plan_build(ncols, nranks, rank, grid, pl);
+    *ntiles = (int32_t)pl.tiles.size();
+    if (tiles)
+        for (int t = 0; t < std::min<int>(cap, (int)pl.tiles.size()); ++t) {
+            const SymTile &T = pl.tiles[t];
+            const int32_t v[8] = {T.r0, T.rows, T.c0, T.cols, T.rslot, T.cmode, T.cbase, T.cslot};
+            std::memcpy(tiles + 8 * t, v, sizeof v);
+        }
+    if (ranges)
+        for (int b = 0; b < grid; ++b) {
+            const SymRange &r = pl.ranges[b];
+            const int32_t v[5] = {r.t0, r.s0, r.t1, r.s1, r.carry};
+            std::memcpy(ranges + 5 * b, v, sizeof v);
+        }
+    if (ldy) *ldy = pl.ldy;
+    if (ldz) *ldz = pl.ldz;
+    return IPM_OK;
+}
 
 #ifdef IPM_TIMELINE
 // diagnostic builds only: the ring of per-iteration kernel timestamps (64 x 8 u64, ns)

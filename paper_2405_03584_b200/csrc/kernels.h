@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "state.h"
 
 namespace ipm {
@@ -19,29 +21,47 @@ constexpr int kSymB = 256;          // symmetric GEMV: square B x B blocks of H
 inline int sym_ncb(int n) { return (n + kSymB - 1) / kSymB; }
 constexpr int kSymSR = 32;          // symmetric GEMV: rows per TMA strip (pipeline stage)
 
-// Strip-balanced work split of the symmetric GEMV.  The strips (kSymSR rows x kSymB columns)
-// of the upper block triangle, in tile order (row-major over tiles I <= J), are cut into
-// `grid` contiguous ranges of equal length, so no CTA streams more than one strip (64 KB)
-// above the average.  A range may start inside a tile: that CTA's column partial of the
-// tile's first (partial) visit goes to an extra "carry" slot nb + carry of the ypart row
-// instead of slot I (which the tile's owner, the CTA holding its strip 0, writes), so every
-// slot is still written by exactly one CTA and the consumers' fixed-order sums stay
-// deterministic.  Returns the number of carry slots K (ypart stride = nb + K).
+// Work plan of the symmetric GEMV (sym_plan_build, linalg.cu).  A tile is a kSymB x kSymB
+// block of this rank's rows; its row part (H_IJ p_J) goes to ypart slot rslot of its rows, its
+// column part (H_IJ^T p_I) to slot cslot of rows cbase.. of ypart (cmode 1) or of the remote
+// buffer zpart (cmode 2: another rank's rows; reduced and exchanged by the caller); cmode 0 =
+// diagonal tile (row part only).  The strips (kSymSR rows) of the tile list are cut into
+// `grid` contiguous equal ranges, so no CTA streams more than one strip (64 KB) above the
+// average.  A range that starts inside a tile writes that tile's column partial to a carry
+// slot (ycarry + k / zcarry + k) instead of cslot (written by the tile's owner, the CTA
+// holding its strip 0): every slot is written by exactly one CTA and the consumers' fixed-
+// order row sums stay deterministic.
+struct SymTile {
+    int r0, rows;   // local rows
+    int c0, cols;   // global columns
+    int rslot;      // ypart slot of the row part
+    int cmode;      // 0 diagonal tile, 1 column part to ypart, 2 column part to zpart
+    int cbase;      // first row (ypart: local row, zpart: compact remote column) of the column part
+    int cslot;      // its slot
+};
 struct SymRange {
-    int t0, s0;     // first tile (upper-triangle row-major index) and first strip in it
+    int t0, s0;     // first tile and first strip in it
     int t1, s1;     // end: tile t1, strip s1 (exclusive); s1 == 0 means the range ends at tile t1
     int carry;      // carry slot of the head partial tile, -1 if none
     int pad[3];
 };
-int sym_partition(int n, int grid, SymRange *out /* grid entries or nullptr */);
+struct SymPlan {
+    std::vector<SymTile> tiles;
+    std::vector<SymRange> ranges;
+    std::vector<int> zcol;          // global column of each zpart row
+    int nbg = 0, ycarry_n = 0, zcarry_n = 0, ldy = 0, ldz = 0, zrows = 0;
+};
+void sym_plan_build(int ncols, int nranks, int rank, int grid, SymPlan &plan);
 
 // linalg.cu
+// sigb_dot (symmetric GEMV only): also add sigma_b p^2 to the fused dot (p^T (H + Sigma_b) p)
 void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb,
-                 double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st);
+                 double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st,
+                 const double *sigb_dot = nullptr);
 int gemv_max_grid();
 bool gemv_bulk_ok(const Prob &P);
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
-                      int grid, int mode, int cid, cudaStream_t st);
+                      int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot = nullptr);
 void launch_count_asym(const Prob &P, unsigned long long *bad, cudaStream_t st);
 bool make_sym_tensor_map(const Prob &P, void *out128);   // CUtensorMap (128 B, 64-B aligned)
 int gemv_bulk_grid();
@@ -52,6 +72,12 @@ void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, 
                  Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid = kMaxGrid,
                  int block = kBlock);
 int num_sms();
+// shard.cu: exchange of the sharded symmetric GEMV's remote column parts, symmetry certificate
+void launch_zreduce(int zrows, int ldz, const double *zpart, const int *zcol, double *zvec, cudaStream_t st);
+void launch_zfold(int nloc, int ncols, int nranks, int64_t row_begin, const double *zall, double *ypart, int ldy,
+                  cudaStream_t st);
+void launch_sym_hash(int nloc, int ncols, int64_t row_begin, int chunk, int nranks, const double *H, int64_t ldh,
+                     unsigned long long *out, cudaStream_t st);
 int side_block();   // CTA size of every PCG-mode SpMV launch (one association => bitwise paths)
 void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
 void configure_pcg_carveout();

@@ -124,7 +124,7 @@ k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
 }
 
 void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb,
-                 double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st) {
+                 double *dpart, Scalars *sc, int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot) {
     const bool vec = ((P.ldh & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.H) & 15) == 0);
     if (P.n == 0) return;
     if (P.hess_compact) {                  // NEXT-1: H p = h0 o p + U (w o (U^T p)), ncb = 1
@@ -132,7 +132,7 @@ void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypa
         return;
     }
     if (P.gemv_sym) {
-        launch_symv_bulk(P, v, vdot, ypart, dpart, sc, P.gemv_bulk_grid, mode, cid, st);
+        launch_symv_bulk(P, v, vdot, ypart, dpart, sc, P.gemv_bulk_grid, mode, cid, st, sigb_dot);
         return;
     }
     if (P.gemv_bulk) {
@@ -399,9 +399,11 @@ bool make_sym_tensor_map(const Prob &P, void *out) {
 
 template <int MODE>
 __global__ void __launch_bounds__(kSymThreads, 1)
-k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__restrict__ p,
-            const double *__restrict__ pdot, double *__restrict__ ypart, int nb, int ldy,
-            const SymRange *__restrict__ ranges, double *__restrict__ dpart, Scalars *sc, int cid, int keep) {
+k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict__ tiles,
+            const SymRange *__restrict__ ranges, const double *__restrict__ p, int64_t row_begin,
+            const double *__restrict__ pdot, double *__restrict__ ypart, int ldy, int ycarry,
+            double *__restrict__ zpart, int ldz, int zcarry, double *__restrict__ dpart, Scalars *sc, int cid,
+            int keep, const double *__restrict__ sigb_dot) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[kSymThreads / 32];
     __shared__ double colbuf[kSymB];                  // row-half-1 column sums of the current tile
@@ -423,8 +425,6 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
     const SymRange rg = ranges[blockIdx.x];
     const int tlast = rg.s1 > 0 ? rg.t1 : rg.t1 - 1;     // last tile touched (inclusive)
     double dacc = 0.0;
-    int I = 0, J = 0;
-    if (rg.t0 <= tlast) sym_locate(rg.t0, nb, I, J);
     if (warp == kSymConsumers) {
         if (lane == 0) {
             uint64_t pol_h, pol_p;
@@ -433,14 +433,13 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
             int stage = 0;
             uint32_t phase = 0;
             for (int t = rg.t0; t <= tlast; ++t) {
-                const int rowsI = min(kSymB, n - I * kSymB);
-                const int colsJ = min(kSymB, n - J * kSymB);
-                const int cwb = (colsJ + 1) & ~1;
+                const SymTile T = tiles[t];
+                const int cwb = (T.cols + 1) & ~1;
                 const int sa = (t == rg.t0) ? rg.s0 : 0;
-                const int sb = (t == rg.t1) ? rg.s1 : (rowsI + kSymSR - 1) / kSymSR;
+                const int sb = (t == rg.t1) ? rg.s1 : (T.rows + kSymSR - 1) / kSymSR;
                 for (int sidx = sa; sidx < sb; ++sidx) {
                     const int s0 = sidx * kSymSR;
-                    const int rows = min(kSymSR, rowsI - s0);
+                    const int rows = min(kSymSR, T.rows - s0);
                     const int rb = (rows + 1) & ~1;
                     mbar_wait(&empty[stage], phase ^ 1u);
                     double *sH = stages + (size_t)stage * kSymStageDoubles;
@@ -448,12 +447,11 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                     double *sPI = sPJ + kSymB;
                     // one 2-D TMA per strip: kSymSR x kSymB box (OOB rows/cols zero-filled, full box bytes)
                     mbar_expect_tx(&full[stage], (uint32_t)((kSymSR * kSymB + cwb + rb) * 8));
-                    tma_2d_g2s(sH, &tmap, J * kSymB, I * kSymB + s0, &full[stage], (t - rg.t0 < keep) ? pol_p : pol_h);
-                    bulk_g2s(sPJ, p + (int64_t)J * kSymB, (uint32_t)(cwb * 8), &full[stage], pol_p);
-                    bulk_g2s(sPI, p + (int64_t)I * kSymB + s0, (uint32_t)(rb * 8), &full[stage], pol_p);
+                    tma_2d_g2s(sH, &tmap, T.c0, T.r0 + s0, &full[stage], (t - rg.t0 < keep) ? pol_p : pol_h);
+                    bulk_g2s(sPJ, p + T.c0, (uint32_t)(cwb * 8), &full[stage], pol_p);
+                    bulk_g2s(sPI, p + row_begin + T.r0 + s0, (uint32_t)(rb * 8), &full[stage], pol_p);
                     if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
                 }
-                if (++J == nb) { ++I; J = I; }
             }
         }
         __syncwarp();
@@ -468,15 +466,15 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
         int stage = 0;
         uint32_t phase = 0;
         for (int t = rg.t0; t <= tlast; ++t) {
-            const int rowsI = min(kSymB, n - I * kSymB);
-            const int colsJ = min(kSymB, n - J * kSymB);
-            const bool diag = (I == J);
+            const SymTile T = tiles[t];
+            const int colsJ = T.cols;
+            const bool diag = (T.cmode == 0);
             const int sa = (t == rg.t0) ? rg.s0 : 0;
-            const int sb = (t == rg.t1) ? rg.s1 : (rowsI + kSymSR - 1) / kSymSR;
+            const int sb = (t == rg.t1) ? rg.s1 : (T.rows + kSymSR - 1) / kSymSR;
             double ce = 0.0, co = 0.0, pj_c = 0.0;
             for (int sidx = sa; sidx < sb; ++sidx) {
                 const int s0 = sidx * kSymSR;
-                const int rows = min(kSymSR, rowsI - s0);
+                const int rows = min(kSymSR, T.rows - s0);
                 mbar_wait(&full[stage], phase);
                 const double *sH = stages + (size_t)stage * kSymStageDoubles;
                 const double *sPJ = sH + kSymSR * kSymB;
@@ -513,13 +511,18 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                     for (int q = 0; q < kSymRW; ++q) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
                 }
                 if (lane == 0) {
-                    const int row = I * kSymB + s0;
+                    const int row = T.r0 + s0;
 #pragma unroll
                     for (int q = 0; q < kSymRW; ++q) {
                         const int r = warp + q * kSymConsumers;
                         if (r < rows) {
-                            ypart[(int64_t)(row + r) * ldy + J] = s[q];
-                            if (pdot) dacc = fma(sPI[r], s[q], dacc);
+                            ypart[(int64_t)(row + r) * ldy + T.rslot] = s[q];
+                            if (pdot) {
+                                dacc = fma(sPI[r], s[q], dacc);
+                                // fused PCG: the diagonal tiles hold every row once, so they also
+                                // add sigma_b p_i^2 — the dot is p^T (H + Sigma_b) p
+                                if (sigb_dot && diag) dacc = fma(sigb_dot[row + r] * sPI[r], sPI[r], dacc);
+                            }
                         }
                     }
                 }
@@ -542,14 +545,19 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
                 consumers_sync();
                 if (h == 0 && c < colsJ) {
                     const double colacc = part + colbuf[c];
-                    // the tile's owner (holds strip 0) writes slot I; a head partial, its carry slot
-                    const int slot = (sa == 0) ? I : nb + rg.carry;
-                    ypart[(int64_t)(J * kSymB + c) * ldy + slot] = colacc;
+                    // the tile's owner (holds strip 0) writes its slot; a head partial, its carry
+                    // slot.  cmode 1: rows of this rank (ypart); cmode 2: another rank's rows (zpart)
+                    if (T.cmode == 1) {
+                        const int slot = (sa == 0) ? T.cslot : ycarry + rg.carry;
+                        ypart[(int64_t)(T.cbase + c) * ldy + slot] = colacc;
+                    } else {
+                        const int slot = (sa == 0) ? T.cslot : zcarry + rg.carry;
+                        zpart[(int64_t)(T.cbase + c) * ldz + slot] = colacc;
+                    }
                     if (pdot) dacc = fma(pj_c, colacc, dacc);
                 }
                 consumers_sync();
             }
-            if (++J == nb) { ++I; J = I; }
         }
     }
     if (pdot == nullptr) return;
@@ -569,39 +577,106 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, int n, const double *__res
 }
 
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
-                      int grid, int mode, int cid, cudaStream_t st) {
+                      int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_symv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
         cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
         attr = true;
     }
-    const int nb = sym_ncb(P.n);
     const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(P.tmap_sym);
     if (mode == 1)
-        k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, P.ncb, P.sym_ranges, dpart, sc,
-                                                             cid, P.sym_keep);
+        k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
+                                                             P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
+                                                             dpart, sc, cid, P.sym_keep, sigb_dot);
     else
-        k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.n, v, vdot, ypart, nb, P.ncb, P.sym_ranges, dpart, sc,
-                                                             cid, P.sym_keep);
+        k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
+                                                             P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
+                                                             dpart, sc, cid, P.sym_keep, sigb_dot);
 }
 
-int sym_partition(int n, int grid, SymRange *out) {
-    const int nb = sym_ncb(n);
-    auto strips = [&](int I) { return (std::min(kSymB, n - I * kSymB) + kSymSR - 1) / kSymSR; };
-    int64_t total = 0;
-    for (int I = 0; I < nb; ++I) total += (int64_t)(nb - I) * strips(I);
-    // walk the tiles once, mapping each range boundary (a global strip index) to (tile, strip)
-    std::vector<int> tI, tJ;
-    std::vector<int64_t> tstart;
-    for (int I = 0; I < nb; ++I)
-        for (int J = I; J < nb; ++J) {
-            tstart.push_back(tstart.empty() ? 0 : tstart.back() + strips(tI.back()));
-            tI.push_back(I);
-            tJ.push_back(J);
+// Work plan of the symmetric GEMV (kernels.h).  Blocks: every rank's rows cut into kSymB
+// blocks from its own row_begin; global block index g(b, k) in rank order.  Rank a reads
+//   * the upper triangle of its diagonal rank-block: tiles (a,I) x (a,J), J >= I — column part
+//     (J > I) into its own ypart rows (cmode 1), diagonal tiles row part only (cmode 0);
+//   * whole off-diagonal rank-blocks H[R_a, R_b] for b = a + d (mod P), 1 <= d <= (P-1)/2, and
+//     for even P the pair at distance P/2 split in two: the lower rank takes b's first
+//     ceil(nb_b / 2) column blocks, the higher rank its own rows from block ceil(nb_a / 2) on
+//     against all of the lower rank's columns.  Their column parts belong to rank b's rows:
+//     written to zpart (cmode 2, row = compact remote column), reduced and exchanged by the caller.
+// Every unordered block pair {(a,I),(b,J)} is read exactly once across ranks, and each rank
+// reads ~ n^2 / (2P) entries.  P = 1 reproduces the single-GPU triangle exactly.
+void sym_plan_build(int ncols, int nranks, int rank, int grid, SymPlan &pl) {
+    const int chunk = (ncols + nranks - 1) / nranks;
+    auto rb = [&](int r) { return std::min<int64_t>((int64_t)r * chunk, ncols); };
+    auto nrows = [&](int r) { return (int)(std::min<int64_t>((int64_t)(r + 1) * chunk, ncols) - rb(r)); };
+    std::vector<int> nbr(nranks), gbase(nranks + 1, 0);
+    for (int r = 0; r < nranks; ++r) {
+        nbr[r] = (nrows(r) + kSymB - 1) / kSymB;
+        gbase[r + 1] = gbase[r] + nbr[r];
+    }
+    const int a = rank, nba = nbr[a];
+    auto bsz = [&](int r, int k) { return std::min(kSymB, nrows(r) - k * kSymB); };
+    pl = SymPlan{};
+    pl.nbg = gbase[nranks];
+    std::vector<std::pair<int, int>> zcols;          // (rank, block) of remote column blocks, Z row order
+    std::vector<int> zbase;
+    auto zrow = [&](int b, int J) {
+        for (size_t q = 0; q < zcols.size(); ++q)
+            if (zcols[q].first == b && zcols[q].second == J) return zbase[q];
+        const int base = zbase.empty() ? 0 : zbase.back() + bsz(zcols.back().first, zcols.back().second);
+        zcols.push_back({b, J});
+        zbase.push_back(base);
+        return base;
+    };
+    std::vector<std::pair<int, int>> remote;        // (rank b, first column block, end block) per row block rule
+    for (int I = 0; I < nba; ++I) {
+        for (int J = I; J < nba; ++J) {
+            SymTile T{};
+            T.r0 = I * kSymB;
+            T.rows = bsz(a, I);
+            T.c0 = (int)rb(a) + J * kSymB;
+            T.cols = bsz(a, J);
+            T.rslot = gbase[a] + J;
+            T.cmode = (I == J) ? 0 : 1;
+            T.cbase = J * kSymB;
+            T.cslot = gbase[a] + I;
+            pl.tiles.push_back(T);
         }
-    const int ntiles = (int)tI.size();
-    auto locate = [&](int64_t g, int &t, int &s) {       // strip g -> (tile, strip), g <= total
+        for (int d = 1; d < nranks; ++d) {
+            const int b = (a + d) % nranks;
+            int j0 = 0, j1 = 0;
+            if (2 * d < nranks) {
+                j1 = nbr[b];
+            } else if (2 * d == nranks) {
+                if (a < b) j1 = (nbr[b] + 1) / 2;
+                else if (I >= (nba + 1) / 2) j1 = nbr[b];
+            }
+            for (int J = j0; J < j1; ++J) {
+                if (nrows(b) <= 0) continue;
+                SymTile T{};
+                T.r0 = I * kSymB;
+                T.rows = bsz(a, I);
+                T.c0 = (int)rb(b) + J * kSymB;
+                T.cols = bsz(b, J);
+                T.rslot = gbase[b] + J;
+                T.cmode = 2;
+                T.cbase = zrow(b, J);
+                T.cslot = I;
+                pl.tiles.push_back(T);
+            }
+        }
+    }
+    pl.zrows = zbase.empty() ? 0 : zbase.back() + bsz(zcols.back().first, zcols.back().second);
+    for (size_t q = 0; q < zcols.size(); ++q)
+        for (int c = 0; c < bsz(zcols[q].first, zcols[q].second); ++c)
+            pl.zcol.push_back((int)rb(zcols[q].first) + zcols[q].second * kSymB + c);
+    // strip-balanced ranges with carry slots (per column target: cmode and base row)
+    const int ntiles = (int)pl.tiles.size();
+    std::vector<int64_t> tstart(ntiles + 1, 0);
+    for (int t = 0; t < ntiles; ++t) tstart[t + 1] = tstart[t] + (pl.tiles[t].rows + kSymSR - 1) / kSymSR;
+    const int64_t total = tstart[ntiles];
+    auto locate = [&](int64_t g, int &t, int &s) {
         if (g >= total) { t = ntiles; s = 0; return; }
         int lo = 0, hi = ntiles - 1;
         while (lo < hi) {
@@ -611,22 +686,31 @@ int sym_partition(int n, int grid, SymRange *out) {
         t = lo;
         s = (int)(g - tstart[lo]);
     };
-    std::vector<int> used(nb, 0);
-    int K = 0;
+    std::vector<std::pair<std::pair<int, int>, int>> used;   // ((cmode, cbase), count)
+    pl.ycarry_n = pl.zcarry_n = 0;
+    pl.ranges.assign(grid, SymRange{});
     for (int b = 0; b < grid; ++b) {
         SymRange r{};
         const int64_t g0 = total * b / grid, g1 = total * (b + 1) / grid;
         locate(g0, r.t0, r.s0);
         locate(g1, r.t1, r.s1);
         r.carry = -1;
-        if (g1 > g0 && r.s0 > 0 && tI[r.t0] != tJ[r.t0]) {
-            r.carry = used[tJ[r.t0]]++;
-            K = std::max(K, r.carry + 1);
+        if (g1 > g0 && r.s0 > 0 && pl.tiles[r.t0].cmode != 0) {
+            const auto key = std::make_pair(pl.tiles[r.t0].cmode, pl.tiles[r.t0].cbase);
+            int k = 0;
+            bool found = false;
+            for (auto &u : used)
+                if (u.first == key) { k = u.second++; found = true; }
+            if (!found) used.push_back({key, 1});
+            r.carry = k;
+            if (key.first == 1) pl.ycarry_n = std::max(pl.ycarry_n, k + 1);
+            else pl.zcarry_n = std::max(pl.zcarry_n, k + 1);
         }
         if (g1 <= g0) { r.t0 = r.t1 = 0; r.s0 = r.s1 = 0; }   // empty range
-        if (out) out[b] = r;
+        pl.ranges[b] = r;
     }
-    return K;
+    pl.ldy = pl.nbg + pl.ycarry_n + (nranks > 1 ? 1 : 0);    // sharded: + the exchanged slot
+    pl.ldz = nba + pl.zcarry_n;
 }
 
 // Exact-symmetry check at create (the symmetric GEMV is only used when H == H^T bitwise).

@@ -335,7 +335,9 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
 // the same stop decision, and — unless stopping — forms p = z + beta p and its S_b partial
 // for the rows it owns, so the next iteration needs no separate k_pcg_p launch.  The scalars
 // are read before the barrier and published by CTA 0 after it.
-template <int G>
+// FOLD: the symmetric GEMV already added sigma_b p^2 to its dot (S_H = p^T (H + Sigma_b) p), so
+// p^T K p = S_H + S_c and the next direction needs no S_b reduction: phase 2 is a plain update.
+template <int G, bool FOLD>
 __global__ void __launch_bounds__(kBlock)
 k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
                 double *__restrict__ p, const double *__restrict__ pAt, double *__restrict__ x,
@@ -347,7 +349,7 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
         return;
     }
-    const double pkp = sc->S_H + sc->S_b + sc->S_c;
+    const double pkp = FOLD ? sc->S_H + sc->S_c : sc->S_H + sc->S_b + sc->S_c;
     if (!(pkp > 0.0) || !finite_d(pkp)) {           // uniform over the grid: nobody waits
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             fin_pcg_alpha(sc, pkp);
@@ -356,6 +358,9 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
         return;
     }
     TL_BEGIN(sc, 3);
+#ifdef IPM_TIMELINE
+    if (threadIdx.x == 0) atomicMax(&sc->tl_u[0], gtimer_ns());
+#endif
     const double rho = sc->rho;
     const double alpha = rho / pkp;
     const int64_t it1 = sc->it + 1, maxit = sc->maxit;
@@ -389,12 +394,18 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
             rr = fma(ri, ri, rr);
         }
     }
+#ifdef IPM_TIMELINE
+    if ((threadIdx.x & 31) == 0) atomicMax(&sc->tl_u[1], gtimer_ns());
+#endif
     const double a = block_sum(rz, red);
     const double b = block_sum(rr, red);
     if (threadIdx.x == 0) {
         p1[blockIdx.x] = a;
         p2[blockIdx.x] = b;
     }
+#ifdef IPM_TIMELINE
+    if (threadIdx.x == 0) atomicMax(&sc->tl_u[2], gtimer_ns());
+#endif
     grid_barrier(&sc->counters[C_BAR], &sc->counters[C_BAR_GEN]);
     const double trz = sum_partials(p1, gridDim.x, red);
     const double trr = sum_partials(p2, gridDim.x, red);
@@ -409,6 +420,10 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
             sc->tl[k][0] = sc->tl[k][1] = 0ull;
         }
         rec[7] = gtimer_ns();                          // update: barrier passed
+        for (int k = 0; k < 3; ++k) {
+            rec[8 + k] = sc->tl_u[k];
+            sc->tl_u[k] = 0ull;
+        }
 #endif
         sc->pKp = pkp;
         sc->alpha = alpha;
@@ -417,6 +432,11 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
     }
     if (stop) return;
     const double beta = trz / rho;
+    if (FOLD) {
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+            p[i] = fma(beta, p[i], __ldcg(z + i));
+        return;
+    }
     // p and its S_b partials with exactly k_pcg_p's association (virtual blocks of kBlock
     // threads over a grid of ceil(n / kBlock)), so the fused and unfused paths agree bitwise
     const int gq = (n + kBlock - 1) / kBlock;
@@ -604,25 +624,25 @@ static void launch_update_g(const Prob &P, const Vecs &V, int /*G*/, int ncb, Sc
 }
 
 // cooperative grid of the fused update: every CTA must be co-resident (grid barrier)
-template <int GG>
+template <int GG, bool FOLD>
 static int fp_grid(int n) {
     static int cap = 0;
     if (!cap) {
         int dev = 0, sms = 0, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_update_fp<GG>, kBlock, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_update_fp<GG, FOLD>, kBlock, 0);
         cap = std::max(1, std::min(occ, 8)) * sms;
     }
     return std::min(grid_for(n, kBlock / GG), cap);
 }
 
-template <int GG>
+template <int GG, bool FOLD>
 static void launch_update_fp_g(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x,
                                cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
     const double *pAt = (P.m > 0) ? V.pAt : nullptr;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(fp_grid<GG>(P.n));
+    cfg.gridDim = dim3(fp_grid<GG, FOLD>(P.n));
     cfg.blockDim = dim3(kBlock);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -630,14 +650,19 @@ static void launch_update_fp_g(const Prob &P, const Vecs &V, int ncb, Scalars *s
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_pcg_update_fp<GG>, P.n, ncb, (const double *)V.ypart, (const double *)V.sig_b, V.pp,
+    cudaLaunchKernelEx(&cfg, k_pcg_update_fp<GG, FOLD>, P.n, ncb, (const double *)V.ypart, (const double *)V.sig_b, V.pp,
                        pAt, x, V.pr, V.pz, (const double *)V.Minv, V.part[5], V.part[6], V.part[2], sc, h, use_cond);
 }
 
 static void launch_update_fp(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x,
-                             cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
-    if (update_group(ncb) == 4) launch_update_fp_g<4>(P, V, ncb, sc, x, h, use_cond, st);
-    else launch_update_fp_g<8>(P, V, ncb, sc, x, h, use_cond, st);
+                             cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, bool fold) {
+    if (fold) {
+        if (update_group(ncb) == 4) launch_update_fp_g<4, true>(P, V, ncb, sc, x, h, use_cond, st);
+        else launch_update_fp_g<8, true>(P, V, ncb, sc, x, h, use_cond, st);
+    } else {
+        if (update_group(ncb) == 4) launch_update_fp_g<4, false>(P, V, ncb, sc, x, h, use_cond, st);
+        else launch_update_fp_g<8, false>(P, V, ncb, sc, x, h, use_cond, st);
+    }
 }
 
 // sharded path: t is complete (replicated on every rank) when this is called
@@ -712,10 +737,12 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
         spmv_stage(P, V, G, sc, st, kMaxGrid, side_block());   // same association as the side branch
         if (!use_cond) dstage("spmv", st);
     }
-    launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st);
+    // fused path with the symmetric GEMV: sigma_b p^2 folded into the GEMV's dot (no S_b pass)
+    const bool fold = fused_p && P.gemv_sym && !P.hess_compact;
+    launch_gemv(P, V.pp, V.pp, V.ypart, ncb, V.part[4], sc, gemv_grid, 1, C_GEMV_PCG, st, fold ? V.sig_b : nullptr);
     if (!use_cond) dstage("gemv", st);
     if (par) cudaStreamWaitEvent(st, fork->ev_join, 0);
-    if (fused_p) launch_update_fp(P, V, ncb, sc, x, h, use_cond, st);
+    if (fused_p) launch_update_fp(P, V, ncb, sc, x, h, use_cond, st, fold);
     else launch_update_g(P, V, G, ncb, sc, x, h, use_cond, st);
 }
 
@@ -726,8 +753,10 @@ void configure_pcg_carveout() {
     cudaFuncSetAttribute(k_spmvT<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_spmvT<16>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_spmvT<32>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-    cudaFuncSetAttribute(k_pcg_update_fp<4>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-    cudaFuncSetAttribute(k_pcg_update_fp<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<4, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<8, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<4, true>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<8, true>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_pcg_update<4>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_pcg_update<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_pcg_update<16>, cudaFuncAttributePreferredSharedMemoryCarveout, c);

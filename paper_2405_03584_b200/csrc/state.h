@@ -55,7 +55,8 @@ struct Scalars {
     // diagnostic builds only (scripts/timeline_probe.py): per-kernel first-CTA start (as ~t)
     // and last thread-0 exit of the current PCG iteration, copied into a ring by the update
     unsigned long long tl[4][2];
-    unsigned long long tl_ring[64][8];
+    unsigned long long tl_u[4];          // update: latest CTA start, latest rows-done, latest arrival
+    unsigned long long tl_ring[64][16];
 #endif
 };
 
@@ -89,7 +90,11 @@ struct Prob {
     int sym_keep;          // leading tiles of each CTA's range loaded with an L2 evict_last policy
     int ncb;               // column blocks of the ypart[row][cb] layout of the chosen GEMV
     const void *tmap_sym;  // host copy of the CUtensorMap over H (16 x 256 fp64 boxes)
-    const struct SymRange *sym_ranges;   // device: per-CTA strip ranges (kernels.h sym_partition)
+    const struct SymRange *sym_ranges;   // device: per-CTA strip ranges (kernels.h SymPlan)
+    const struct SymTile *sym_tiles;     // device: the tile list
+    double *sym_z;                       // sharded: column parts of other ranks' rows [zrows][ldz]
+    int sym_ycarry, sym_ldz, sym_zcarry; // ypart carry base (= nbg), zpart stride and carry base
+    int64_t row_begin;                   // global index of local row 0
     // compact quasi-Newton Hessian H = diag(h0) + U diag(w) U^T (compact.cu)
     int hess_compact;
     int ck;                // columns of U in use

@@ -18,9 +18,15 @@ q = config(wl, 0)
 t = problem_tensors(q, torch.device("cuda", 0))
 qp = QP(device="cuda:0", max_ipm_iter=1, pcg_max_iter=20, **t)
 qp.solve()
-res = {"workload": wl, "upd_g": os.environ.get("IPM_UPD_G"), "keep_mb": os.environ.get("IPM_SYM_KEEP_MB"),
+res = {"workload": wl, "upd_g": os.environ.get("IPM_UPD_G"), "unroll": os.environ.get("IPM_UNROLL"), "keep_mb": os.environ.get("IPM_SYM_KEEP_MB"),
        "persist_mb": os.environ.get("PERSIST_MB"), "gemv_ms": qp.profile("gemv", 30),
        "spmv_ms": qp.profile("spmv", 30) if q.m else None, "pcg_iter_ms": qp.profile("pcg_iter", 30)}
+qg = QP(device="cuda:0", max_ipm_iter=1, pcg_max_iter=300, **t)   # captured-graph PCG iterations
+qg.solve()
+qg.solve()
+sg = qg.stats()
+res["graph_pcg_iter_ms"] = sg["t_pcg_ms"] / max(1, sg["pcg_iters_total"])
+qg.close()
 if os.environ.get("PROBE_QP", "1") == "0":
     print(json.dumps(res), flush=True)
     sys.exit(0)

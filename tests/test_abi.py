@@ -119,3 +119,63 @@ def test_sqp_struct_sizes_match_c(lib, tmp_path):
     o = lib.ipm_sqp_options()
     lib.ipm_sqp_options_default(C.byref(o))
     assert o.size == C.sizeof(lib.ipm_sqp_options) and o.max_iter == 50 and o.tol_d == 1e-6 and o.powell == 0.2
+
+
+def _sym_plan(lib, n, P, r, grid):
+    nt = C.c_int32()
+    ldy, ldz = C.c_int32(), C.c_int32()
+    assert lib.ipm_sym_plan(n, P, r, grid, None, 0, C.byref(nt), None, None, None) == 0
+    tiles = (C.c_int32 * (8 * nt.value))()
+    ranges = (C.c_int32 * (5 * grid))()
+    assert lib.ipm_sym_plan(n, P, r, grid, tiles, nt.value, C.byref(nt), ranges, C.byref(ldy), C.byref(ldz)) == 0
+    import numpy as np
+    return (np.array(tiles, dtype=np.int64).reshape(-1, 8), np.array(ranges, dtype=np.int64).reshape(-1, 5),
+            ldy.value, ldz.value)
+
+
+@pytest.mark.parametrize("n,P,grid", [(1000, 1, 148), (1000, 2, 148), (1000, 3, 7), (1000, 4, 148), (777, 5, 31),
+                                      (300, 8, 148), (2600, 6, 148), (20000, 1, 148)])
+def test_sym_plan_uses_every_entry_once(lib, n, P, grid):
+    """Host-side work plan of the (sharded) symmetric GEMV (NEXT-3 + SURVEY §8(e)): across all
+    ranks, every ORDERED entry (i, j) of H enters y = H p exactly once — as a row part of a tile
+    holding row i, or as the column part of a tile holding (j, i) — and each rank's strip ranges
+    cover its tiles' strips exactly once, in order.  Pinned by counting, no GPU needed."""
+    import numpy as np
+    chunk = -(-n // P)
+    small = n <= 3000
+    used = np.zeros((n, n), dtype=np.int32) if small else None
+    per_rank = []
+    for r in range(P):
+        rb = min(r * chunk, n)
+        tiles, ranges, ldy, ldz = _sym_plan(lib, n, P, r, grid)
+        reads = 0
+        for r0, rows, c0, cols, rslot, cmode, cbase, cslot in tiles:
+            gi0 = rb + r0
+            assert 0 < rows <= 256 and 0 < cols <= 256 and 0 <= c0 and c0 + cols <= n
+            reads += rows * cols
+            if small:
+                used[gi0:gi0 + rows, c0:c0 + cols] += 1                     # row part
+                if cmode != 0:
+                    used[c0:c0 + cols, gi0:gi0 + rows] += 1                 # column part (H symmetric)
+            if cmode == 0:
+                assert c0 == gi0 and cols == rows
+            if cmode == 1:
+                assert rb <= c0 and c0 + cols <= rb + chunk and cbase == c0 - rb
+        per_rank.append(reads)
+        # ranges: contiguous, in order, covering every strip once
+        strips = [(t[1] + 31) // 32 for t in tiles]
+        pos = 0
+        flat = [(t, s) for t in range(len(tiles)) for s in range(strips[t])]
+        for t0, s0, t1, s1, carry in ranges:
+            a = flat.index((t0, s0)) if (t0, s0) != (len(tiles), 0) and t0 < len(tiles) else len(flat)
+            b = flat.index((t1, s1)) if t1 < len(tiles) else len(flat)
+            if t0 == t1 and s0 == s1:
+                continue
+            assert a == pos
+            pos = b
+            assert (carry >= 0) == (s0 > 0 and tiles[t0][5] != 0)
+        assert pos == len(flat)
+    if small:
+        assert used.min() == 1 and used.max() == 1
+    # balanced: every rank streams about n^2 / (2P) entries
+    assert max(per_rank) <= 1.15 * n * n / (2 * P) + 256 * 256 * 4

@@ -15,17 +15,19 @@ pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda", 0) if torch.cuda.is_available() else None
 
 
-def _sharded(q, P, **opts):
+def _sharded(q, P, H=None, **opts):
     from paper_2405_03584_b200 import QP
     from paper_2405_03584_b200.dist import LocalGroup, partition
-    t = problem_tensors(q, DEV)
+    t = problem_tensors(q, DEV) if H is None else dict(problem_tensors(q, DEV), H=H)
     grp = LocalGroup(P)
-    qps = []
+    fns = []
     for r, (b, e) in enumerate(partition(q.n, P)):
         tr = dict(t)
         tr["H"] = t["H"][b:e].contiguous()
-        qps.append(QP(device=DEV, stream=torch.cuda.Stream(DEV), shard=grp.shard(r), **tr, **opts))
-    return grp, qps
+        fns.append(lambda r=r, tr=tr: QP(device=DEV, stream=torch.cuda.Stream(DEV), shard=grp.shard(r), **tr, **opts))
+    # ipm_create is collective when sharded (the symmetry certificate is exchanged): every
+    # rank's context is created concurrently, as separate processes would under NCCL
+    return grp, grp.run(fns)
 
 
 def _solve_all(grp, qps):
@@ -102,3 +104,59 @@ def test_sharded_op_apply_rows():
     y = torch.cat(ys).cpu().numpy()
     yref = okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v, dtype=np.longdouble).astype(np.float64)
     assert np.linalg.norm(y - yref) <= 1e-12 * np.linalg.norm(yref)
+
+
+@pytest.mark.parametrize("n,P", [(1000, 2), (1200, 3), (1000, 4), (2600, 5)])
+def test_sharded_symmetric_op_apply(n, P):
+    """Row-sharded symmetric GEMV (each rank reads ~n^2/(2P) entries of its row block; the
+    column parts of other ranks' rows are exchanged): K v matches a longdouble reference."""
+    q = planted_qp(n, 300, density=0.02, rank=32, seed=n + P, rows="mixed")
+    grp, qps = _sharded(q, P)
+    assert all(qq.info()["gemv_kernel"] == 3 for qq in qps)          # chunk even: symmetric path
+    rng = np.random.default_rng(P)
+    sb, sc, v = rng.uniform(0, 2, q.n), 10 ** rng.uniform(-2, 2, q.m), rng.normal(size=q.n)
+    from paper_2405_03584_b200.dist import partition
+    ys = grp.run([lambda r=r, qq=qq: qq.op_apply(sb[slice(*partition(q.n, P)[r])], sc, v)
+                  for r, qq in enumerate(qps)])
+    y = torch.cat(ys).cpu().numpy()
+    yref = okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v, dtype=np.longdouble).astype(np.float64)
+    assert np.linalg.norm(y - yref) <= 1e-12 * np.linalg.norm(yref)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_symmetric_matches_oracle_and_is_reproducible(P):
+    q = planted_qp(1000, 300, density=0.02, rank=32, seed=60 + P, rows="vmat", var="box")
+    runs = []
+    for _ in range(2):
+        grp, qps = _sharded(q, P)
+        assert all(qq.info()["gemv_kernel"] == 3 for qq in qps)
+        runs.append(_solve_all(grp, qps))
+    (st, x, stats), (_, x2, _) = runs
+    assert st == ["ok"] * P and np.array_equal(x, x2)
+    ref = solve(Problem.from_data(q))
+    assert np.max(np.abs(x - ref.x)) <= 1e-6 * max(1.0, np.max(np.abs(ref.x)))
+    assert len({s["obj"] for s in stats}) == 1
+    assert abs(stats[0]["obj"] - ref.obj) <= 1e-8 * abs(ref.obj)
+    assert abs(stats[0]["ipm_iters"] - ref.iters) <= 2
+
+
+def test_sharded_asymmetric_H_falls_back_on_every_rank():
+    """One off-diagonal entry changed on ONE side (rank 1's rows only): the exchanged hash
+    certificate fails on every rank, so all ranks take the full GEMV (auto) and
+    gemv_kernel=3 is refused; the full GEMV stays exact for the stored (asymmetric) H."""
+    from paper_2405_03584_b200 import _lib
+    q = planted_qp(1000, 100, density=0.02, rank=16, seed=3)
+    H = problem_tensors(q, DEV)["H"].clone()
+    H[700, 10] += 1e-3                      # row 700 belongs to rank 1 of 2; H[10, 700] unchanged
+    grp, qps = _sharded(q, 2, H=H)
+    assert all(qq.info()["gemv_kernel"] != 3 for qq in qps)
+    rng = np.random.default_rng(0)
+    sb, sc, v = rng.uniform(0, 2, q.n), 10 ** rng.uniform(-2, 2, q.m), rng.normal(size=q.n)
+    from paper_2405_03584_b200.dist import partition
+    ys = grp.run([lambda r=r, qq=qq: qq.op_apply(sb[slice(*partition(q.n, 2)[r])], sc, v)
+                  for r, qq in enumerate(qps)])
+    Hn = H[:, :q.n].cpu().numpy()
+    yref = okkt.condensed_apply(Hn, q.A_dense(), sb, sc, v, dtype=np.longdouble).astype(np.float64)
+    assert np.linalg.norm(torch.cat(ys).cpu().numpy() - yref) <= 1e-12 * np.linalg.norm(yref)
+    with pytest.raises(_lib.IpmError, match="symmetric"):
+        _sharded(q, 2, H=H, gemv_kernel=3)
