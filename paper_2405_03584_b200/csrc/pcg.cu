@@ -337,14 +337,14 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
 // are read before the barrier and published by CTA 0 after it.
 // FOLD: the symmetric GEMV already added sigma_b p^2 to its dot (S_H = p^T (H + Sigma_b) p), so
 // p^T K p = S_H + S_c and the next direction needs no S_b reduction: phase 2 is a plain update.
-template <int G, bool FOLD>
-__global__ void __launch_bounds__(kBlock)
+template <int G, bool FOLD, int BS>
+__global__ void __launch_bounds__(BS)
 k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
                 double *__restrict__ p, const double *__restrict__ pAt, double *__restrict__ x,
                 double *__restrict__ r, double *__restrict__ z, const double *__restrict__ Minv,
                 double *__restrict__ p1, double *__restrict__ p2, double *__restrict__ p3, Scalars *sc,
                 cudaGraphConditionalHandle h, int use_cond) {
-    __shared__ double red[kBlock / 32];
+    __shared__ double red[BS / 32];
     if (sc->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
         return;
@@ -624,44 +624,54 @@ static void launch_update_g(const Prob &P, const Vecs &V, int /*G*/, int ncb, Sc
 }
 
 // cooperative grid of the fused update: every CTA must be co-resident (grid barrier)
-template <int GG, bool FOLD>
+template <int GG, bool FOLD, int BS>
 static int fp_grid(int n) {
     static int cap = 0;
     if (!cap) {
         int dev = 0, sms = 0, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_update_fp<GG, FOLD>, kBlock, 0);
-        cap = std::max(1, std::min(occ, 8)) * sms;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_update_fp<GG, FOLD, BS>, BS, 0);
+        cap = std::max(1, std::min(occ, 2048 / BS)) * sms;
     }
-    return std::min(grid_for(n, kBlock / GG), cap);
+    return std::min(grid_for(n, BS / GG), cap);
 }
 
-template <int GG, bool FOLD>
+template <int GG, bool FOLD, int BS>
 static void launch_update_fp_g(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x,
                                cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
     const double *pAt = (P.m > 0) ? V.pAt : nullptr;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(fp_grid<GG, FOLD>(P.n));
-    cfg.blockDim = dim3(kBlock);
+    cfg.gridDim = dim3(fp_grid<GG, FOLD, BS>(P.n));
+    cfg.blockDim = dim3(BS);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_pcg_update_fp<GG, FOLD>, P.n, ncb, (const double *)V.ypart, (const double *)V.sig_b, V.pp,
+    cudaLaunchKernelEx(&cfg, k_pcg_update_fp<GG, FOLD, BS>, P.n, ncb, (const double *)V.ypart, (const double *)V.sig_b, V.pp,
                        pAt, x, V.pr, V.pz, (const double *)V.Minv, V.part[5], V.part[6], V.part[2], sc, h, use_cond);
 }
 
 static void launch_update_fp(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x,
                              cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, bool fold) {
-    if (fold) {
-        if (update_group(ncb) == 4) launch_update_fp_g<4, true>(P, V, ncb, sc, x, h, use_cond, st);
-        else launch_update_fp_g<8, true>(P, V, ncb, sc, x, h, use_cond, st);
+    // CTA size 256 (the S_b association of k_pcg_p); IPM_UPD_BIG=1 tries 1024-thread CTAs for
+    // the FOLD variant (fewer partials after the barrier) — measured no faster at C3
+    static int big = -1;
+    if (big < 0) {
+        const char *e = getenv("IPM_UPD_BIG");
+        big = e ? atoi(e) : 0;       // measured: 1024-thread CTAs no faster at C3 (timeline)
+    }
+    if (fold && big) {
+        if (update_group(ncb) == 4) launch_update_fp_g<4, true, 1024>(P, V, ncb, sc, x, h, use_cond, st);
+        else launch_update_fp_g<8, true, 1024>(P, V, ncb, sc, x, h, use_cond, st);
+    } else if (fold) {
+        if (update_group(ncb) == 4) launch_update_fp_g<4, true, kBlock>(P, V, ncb, sc, x, h, use_cond, st);
+        else launch_update_fp_g<8, true, kBlock>(P, V, ncb, sc, x, h, use_cond, st);
     } else {
-        if (update_group(ncb) == 4) launch_update_fp_g<4, false>(P, V, ncb, sc, x, h, use_cond, st);
-        else launch_update_fp_g<8, false>(P, V, ncb, sc, x, h, use_cond, st);
+        if (update_group(ncb) == 4) launch_update_fp_g<4, false, kBlock>(P, V, ncb, sc, x, h, use_cond, st);
+        else launch_update_fp_g<8, false, kBlock>(P, V, ncb, sc, x, h, use_cond, st);
     }
 }
 
@@ -753,10 +763,12 @@ void configure_pcg_carveout() {
     cudaFuncSetAttribute(k_spmvT<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_spmvT<16>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_spmvT<32>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-    cudaFuncSetAttribute(k_pcg_update_fp<4, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-    cudaFuncSetAttribute(k_pcg_update_fp<8, false>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-    cudaFuncSetAttribute(k_pcg_update_fp<4, true>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-    cudaFuncSetAttribute(k_pcg_update_fp<8, true>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<4, false, kBlock>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<8, false, kBlock>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<4, true, kBlock>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<8, true, kBlock>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<4, true, 1024>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaFuncSetAttribute(k_pcg_update_fp<8, true, 1024>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_pcg_update<4>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_pcg_update<8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
     cudaFuncSetAttribute(k_pcg_update<16>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
