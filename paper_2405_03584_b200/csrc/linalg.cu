@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -355,17 +356,6 @@ __device__ __forceinline__ void consumers_sync() {      // named barrier 1: cons
     asm volatile("bar.sync 1, %0;" ::"n"(kSymConsumers * 32) : "memory");
 }
 
-__device__ __forceinline__ void sym_locate(int64_t t, int nb, int &I, int &J) {
-    int i = 0;
-    int64_t c = 0;
-    while (c + (nb - i) <= t) {
-        c += nb - i;
-        ++i;
-    }
-    I = i;
-    J = i + (int)(t - c);
-}
-
 __device__ __forceinline__ void tma_2d_g2s(void *dst, const CUtensorMap *tmap, int x, int y, uint64_t *bar,
                                            uint64_t pol) {
     asm volatile(
@@ -671,6 +661,19 @@ void sym_plan_build(int ncols, int nranks, int rank, int grid, SymPlan &pl) {
     for (size_t q = 0; q < zcols.size(); ++q)
         for (int c = 0; c < bsz(zcols[q].first, zcols[q].second); ++c)
             pl.zcol.push_back((int)rb(zcols[q].first) + zcols[q].second * kSymB + c);
+    // Interleaved order (IPM_SYM_ORDER=1, experiment): CTA b's contiguous range holds the tiles
+    // b, b + grid, b + 2 grid, ... of the row-major order, so at any moment all CTAs stream the
+    // same few block rows (a shared TLB working set) instead of 148 distant regions.
+    {
+        const char *e = getenv("IPM_SYM_ORDER");
+        if (e && atoi(e) == 1 && (int)pl.tiles.size() > grid) {
+            std::vector<SymTile> perm;
+            perm.reserve(pl.tiles.size());
+            for (int b = 0; b < grid; ++b)
+                for (size_t t = b; t < pl.tiles.size(); t += grid) perm.push_back(pl.tiles[t]);
+            pl.tiles.swap(perm);
+        }
+    }
     // strip-balanced ranges with carry slots (per column target: cmode and base row)
     const int ntiles = (int)pl.tiles.size();
     std::vector<int64_t> tstart(ntiles + 1, 0);

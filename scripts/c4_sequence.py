@@ -42,8 +42,11 @@ for k in range(a.K):
     st = qp.solve()
     s = qp.stats()
     tot_ms += s["t_solve_ms"]
+    fstar = q.f_star if k == 0 else ups[k - 1].f_star
+    x = qp.solution()["x"].cpu().numpy()
     rec = {"qp": k, "status": st, "t_solve_s": s["t_solve_ms"] / 1e3, "ipm": s["ipm_iters"],
-           "pcg": s["pcg_iters_total"], "obj": s["obj"]}
+           "pcg": s["pcg_iters_total"], "obj": s["obj"], "rel_err_f_planted": abs(s["obj"] - fstar) / abs(fstar),
+           "max_err_x_planted": float(abs(x - q.x_star).max())}
     rows.append(rec)
     print(json.dumps(rec), flush=True)
 print(json.dumps({"summary": "C4", "K": a.K, "mode": "cold" if a.cold else "warm", "n": q.n, "m": q.m,

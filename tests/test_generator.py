@@ -58,3 +58,20 @@ def test_generator_is_pure():
     b = config("C1", 4)
     for f in ("g", "A_val", "l", "u", "xl", "xu", "x_star"):
         assert np.array_equal(getattr(a, f), getattr(b, f))
+
+
+def test_c4_sequence_stays_planted():
+    """after every BFGS rank-2 update of H the planted formula re-derives g_k,
+    so the planted x* is the exact optimum of each QP of the sequence — checked by the oracle
+    (x* and f*_k within its duality-gap error)."""
+    from gen.sqp_sequence import apply_dense, sqp_sequence
+    from oracle.ipm import Problem, solve
+    q = planted_qp(300, 80, density=0.05, rank=16, seed=3, rows="vmat", var="box")
+    ups = sqp_sequence(q, 4, seed=0)
+    H = q.H.copy()
+    for up in ups:
+        apply_dense(H, up)
+        r = solve(Problem(H=H, g=up.g.copy(), A=q.A_scipy(), l=q.l, u=q.u, xl=q.xl, xu=q.xu))
+        assert r.status == "converged"
+        assert np.max(np.abs(r.x - q.x_star)) <= 1e-6
+        assert abs(r.obj - up.f_star) <= 1e-8 * abs(up.f_star)

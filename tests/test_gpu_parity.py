@@ -303,3 +303,21 @@ def test_invalid_inputs_rejected():
     bad["H"] = H
     with pytest.raises(_lib.IpmError, match="non-finite"):
         QP(device=DEV, **bad)
+
+
+@pytest.mark.parametrize("n,m", [(300, 0), (2049, 500), (12000, 0)])
+def test_symmetric_gemv_interleaved_order(n, m, monkeypatch):
+    """IPM_SYM_ORDER=1: the same tiles in an interleaved per-CTA order (and so different carry
+    splits) — K v still matches the longdouble reference, and bitwise on dyadic inputs."""
+    monkeypatch.setenv("IPM_SYM_ORDER", "1")
+    q = planted_qp(n, m, density=min(1.0, 0.02 + 2.0 / n), rank=min(48, n), seed=n + 3 * m,
+                   rows="mixed" if m else "vmat", var="mixed")
+    if m:
+        q.A_val = np.round(q.A_val * 16) / 16.0
+    qp = _qp(q, gemv_kernel=3)
+    sb, sc, v = _rand_sigmas(q, 4)
+    y = qp.op_apply(sb, sc, v).cpu().numpy()
+    yref = okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v, dtype=np.longdouble).astype(np.float64)
+    assert np.linalg.norm(y - yref) <= 1e-12 * np.linalg.norm(yref)
+    sb, sc, v = _rand_sigmas(q, 5, dyadic=True)
+    assert np.array_equal(qp.op_apply(sb, sc, v).cpu().numpy(), okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v))
