@@ -29,7 +29,8 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
     """variant "tl": diagnostic build with per-kernel timeline stamps (-DIPM_TIMELINE) into
     libipm_tl.so; loaded only when IPM_LIB points at it (scripts/timeline_probe.py)."""
     lib = LIB if not variant else LIB.replace("libipm.so", f"libipm_{variant}.so")
-    extra = ["-DIPM_TIMELINE"] if variant == "tl" else []
+    extra = {"tl": ["-DIPM_TIMELINE"], "sr16": ["-DIPM_SYM_SR=16", "-DIPM_SYM_STAGES=6"],
+             "sr16s4": ["-DIPM_SYM_SR=16", "-DIPM_SYM_STAGES=4"]}.get(variant, [])
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers += [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
     objdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))
@@ -61,4 +62,5 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, variant="tl" if "--timeline" in sys.argv else ""))
+    var = "tl" if "--timeline" in sys.argv else next((a[10:] for a in sys.argv if a.startswith("--variant=")), "")
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, variant=var))

@@ -19,7 +19,10 @@ constexpr int kGemvCW = 1024;       // columns per GEMV tile (8 KB of the vector
 inline int gemv_ncb(int ncols) { return (ncols + kGemvCW - 1) / kGemvCW; }
 constexpr int kSymB = 256;          // symmetric GEMV: square B x B blocks of H
 inline int sym_ncb(int n) { return (n + kSymB - 1) / kSymB; }
-constexpr int kSymSR = 32;          // symmetric GEMV: rows per TMA strip (pipeline stage)
+#ifndef IPM_SYM_SR
+#define IPM_SYM_SR 32
+#endif
+constexpr int kSymSR = IPM_SYM_SR;  // symmetric GEMV: rows per TMA strip (pipeline stage)
 
 // Work plan of the symmetric GEMV (sym_plan_build, linalg.cu).  A tile is a kSymB x kSymB
 // block of this rank's rows; its row part (H_IJ p_J) goes to ypart slot rslot of its rows, its

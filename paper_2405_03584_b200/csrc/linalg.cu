@@ -344,7 +344,10 @@ void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double
 // the tile and accumulates its column part over the strips in a register; warp w reduces
 // rows w and w+8 of each strip.  Tiles (row-major over the upper triangle) are split among
 // the persistent CTAs as contiguous ranges.
-constexpr int kSymStages = 3;
+#ifndef IPM_SYM_STAGES
+#define IPM_SYM_STAGES 3
+#endif
+constexpr int kSymStages = IPM_SYM_STAGES;
 constexpr int kSymConsumers = 16;                 // consumer warps (2 per strip row pair)
 constexpr int kSymThreads = 32 * (kSymConsumers + 1);
 constexpr int kSymRW = kSymSR / kSymConsumers;    // strip rows reduced by each consumer warp
@@ -661,12 +664,13 @@ void sym_plan_build(int ncols, int nranks, int rank, int grid, SymPlan &pl) {
     for (size_t q = 0; q < zcols.size(); ++q)
         for (int c = 0; c < bsz(zcols[q].first, zcols[q].second); ++c)
             pl.zcol.push_back((int)rb(zcols[q].first) + zcols[q].second * kSymB + c);
-    // Interleaved order (IPM_SYM_ORDER=1, experiment): CTA b's contiguous range holds the tiles
-    // b, b + grid, b + 2 grid, ... of the row-major order, so at any moment all CTAs stream the
-    // same few block rows (a shared TLB working set) instead of 148 distant regions.
+    // Interleaved order (default; IPM_SYM_ORDER=0 restores row-major ranges): CTA b's contiguous
+    // range holds the tiles b, b + grid, b + 2 grid, ... of the row-major order, so at any moment
+    // all CTAs stream the same few block rows (a shared TLB working set) instead of 148 distant
+    // regions.  Measured: C5 SYMV 6.18 -> 6.51 TB/s, C3 6.57 -> 6.62 TB/s (r01_symv_order.jsonl).
     {
         const char *e = getenv("IPM_SYM_ORDER");
-        if (e && atoi(e) == 1 && (int)pl.tiles.size() > grid) {
+        if (!(e && atoi(e) == 0) && (int)pl.tiles.size() > grid) {
             std::vector<SymTile> perm;
             perm.reserve(pl.tiles.size());
             for (int b = 0; b < grid; ++b)
