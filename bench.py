@@ -9,9 +9,12 @@ patient-case-shaped QP (n=20000, m=5000, 1% dense A, dense 3.2 GB H) — see DES
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl ours|reference]
 
 value = QPs solved per second over the whole job (all ranks) = N*K / max-over-ranks time.
-N > 1 solves ONE QP row-sharded over the N GPUs (NCCL allgathers inside libipm; "scaling":
-"strong"); --replicas runs N independent QPs instead ("weak").  --impl reference times the CPU oracle (oracle/) as it
-stands on the host cores, on a bounded sample (one IPM iteration per step) scaled to QP/s.
+N > 1: a workload that fits one GPU (C1-C3) runs as N independent replicas —
+rank r solves the QP of seed + r, no data-path collective ("scaling": "weak"); C5 (80 GB H) is
+solved as ONE QP row-sharded over the N GPUs (NCCL allgathers inside libipm, "strong").
+--shard forces the row-sharded path for any workload (and at N = 1).  --impl reference times
+the CPU oracle (oracle/) as it stands on the host cores, on a bounded sample (one IPM iteration
+per step) scaled to QP/s.
 """
 from __future__ import annotations
 
@@ -174,11 +177,12 @@ def run_ours(args):
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    q = config(args.workload, args.seed)
+    # C5 at N > 1 (or --shard): ONE QP row-sharded over the ranks (NCCL allgathers inside libipm,
+    # SURVEY §8(e)), each rank building only its row block of H on its device; otherwise every
+    # rank solves its own QP (seed + rank): replicas, no collective on the data path.
+    sharded = (ws > 1 and args.workload == "C5") or args.force_shard
+    q = config(args.workload, args.seed if sharded else args.seed + rank)
     n, m, nnz = q.n, q.m, q.nnz
-    # N > 1: ONE QP row-sharded over the ranks (NCCL allgathers inside libipm),
-    # each rank building only its row block of H on its device; --replicas: N independent QPs.
-    sharded = (ws > 1 or args.force_shard) and not args.replicas
     extra = {"use_graph": 0} if args.host_loop else {}
     rows = (0, n)
     if sharded:
@@ -247,14 +251,19 @@ def run_ours(args):
     pcg_iter_ms = qp.profile("pcg_iter", reps=10 if n >= 10000 else 50)
     ncb = info["ncb"]
     if info["gemv_kernel"] == 3:
-        # symmetric GEMV streams the upper block triangle of H (kSymB = 256 blocks, diagonal
-        # blocks whole): algorithmic bytes = 8 * sum over tiles I <= J of rows_I * cols_J
-        B = 256
-        nb = (n + B - 1) // B            # ncb = nb + the carry slots of the strip-balanced split
-        sizes = [min(B, n - i * B) for i in range(nb)]
-        tri = sum(sizes[i] * sizes[j] for i in range(nb) for j in range(i, nb))
-        gemv_bytes = 8.0 * tri + 8.0 * n + 8.0 * n * ncb
-        kname = "k_symv_bulk<1> (symmetric upper-triangle GEMV, 2-D TMA, p^T H p fused)"
+        # symmetric GEMV: algorithmic bytes = the tiles this rank streams (its share of the upper
+        # block triangle, from the library's own work plan) + p + the tile partials
+        import ctypes as C
+        from paper_2405_03584_b200 import _lib
+        nt = C.c_int32()
+        _lib.ipm_sym_plan(n, ws if sharded else 1, rank if sharded else 0, 148, None, 0, C.byref(nt), None, None, None)
+        tl = (C.c_int32 * (8 * nt.value))()
+        _lib.ipm_sym_plan(n, ws if sharded else 1, rank if sharded else 0, 148, tl, nt.value, C.byref(nt), None,
+                          None, None)
+        elems = sum(tl[8 * t + 1] * tl[8 * t + 3] for t in range(nt.value))
+        nrow = rows[1] - rows[0]
+        gemv_bytes = 8.0 * elems + 8.0 * n + 8.0 * nrow * ncb
+        kname = "k_symv_bulk<1> (symmetric upper-triangle GEMV, 2-D TMA, p^T (H + Sigma_b) p fused)"
     else:
         nrow = rows[1] - rows[0]
         gemv_bytes = 8.0 * nrow * n + 8.0 * n + 8.0 * nrow * ncb   # H (local rows) + p + tile partials
@@ -334,7 +343,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic planted-KKT QP (gen/planted.py, seeded; random-init dyadic H = diag + U W U^T)",
-            "config": {"workload": args.workload, **CONFIGS[args.workload], "seed": args.seed, "nnz": nnz,
+            "config": {"workload": args.workload, **CONFIGS[args.workload],
+                       "seed": args.seed if (sharded or ws == 1) else f"{args.seed}..{args.seed + ws - 1} (one per rank)", "nnz": nnz,
                        "H_bytes": 8 * n * n, "l2": "inputs larger than L2 (H >> 126 MB), no flush",
                        "parallelism": (f"row-sharded H over {ws} GPUs (NCCL allgather)" if sharded
                                        else (f"replicas x{ws}" if ws > 1 else "1 GPU"))},
@@ -374,8 +384,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--replicas", action="store_true", help="N>1: N independent QPs instead of one sharded QP")
-    ap.add_argument("--force-shard", action="store_true", help="N=1: run the NCCL row-sharded code path")
+    ap.add_argument("--shard", "--force-shard", dest="force_shard", action="store_true",
+                    help="row-shard ONE QP over the N ranks (default only for C5) — also at N = 1 (NCCL path)")
     ap.add_argument("--no-extra", action="store_true", help="skip the C1/C2 context timings")
     ap.add_argument("--host-loop", action="store_true",
                     help="profiling only: drive the PCG from the host (batches of 16) instead of the conditional-"
