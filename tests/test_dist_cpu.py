@@ -41,8 +41,27 @@ def _worker(rank, world, port, q):
         parts = [None] * world
         dist.all_gather_object(parts, x_loc)
         x = np.concatenate(parts)
+        # sharded symmetric GEMV: each rank derives ITS work plan (host-only library hook); the
+        # gathered plans use every ordered entry (i, j) of H exactly once across the world
+        import ctypes as C
+        from paper_2405_03584_b200 import _lib
+        nsym = 1000
+        nt = C.c_int32()
+        _lib.ipm_sym_plan(nsym, world, rank, 148, None, 0, C.byref(nt), None, None, None)
+        tl = (C.c_int32 * (8 * nt.value))()
+        _lib.ipm_sym_plan(nsym, world, rank, 148, tl, nt.value, C.byref(nt), None, None, None)
+        plans = [None] * world
+        dist.all_gather_object(plans, (min(rank * -(-nsym // world), nsym), list(tl)))
+        used = np.zeros((nsym, nsym), dtype=np.int32)
+        for rb, flat in plans:
+            for t in range(len(flat) // 8):
+                r0, rows, c0, cols, _, cmode, _, _ = flat[8 * t:8 * t + 8]
+                used[rb + r0:rb + r0 + rows, c0:c0 + cols] += 1
+                if cmode != 0:
+                    used[c0:c0 + cols, rb + r0:rb + r0 + rows] += 1
+        sym_ok = bool(used.min() == 1 and used.max() == 1)
         q.put((rank, ok_same, tiles, uid == bytes(range(128)) and len(uid) == NCCL_UNIQUE_ID_BYTES,
-               bool(np.array_equal(x, np.arange(n) / n))))
+               bool(np.array_equal(x, np.arange(n) / n)) and sym_ok))
     finally:
         dist.destroy_process_group()
 
