@@ -81,7 +81,8 @@ void launch_zfold(int nloc, int ncols, int nranks, int64_t row_begin, const doub
                   cudaStream_t st);
 void launch_sym_hash(int nloc, int ncols, int64_t row_begin, int chunk, int nranks, const double *H, int64_t ldh,
                      unsigned long long *out, cudaStream_t st);
-int side_block();   // CTA size of every PCG-mode SpMV launch (one association => bitwise paths)
+int side_block();
+int spmv_keep();    // 1: PCG-mode SpMV / SpMV^T load A, A^T with an L2 evict_last priority   // CTA size of every PCG-mode SpMV launch (one association => bitwise paths)
 void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
 void configure_pcg_carveout();
 // NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,

@@ -750,7 +750,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kBlock)
 k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const double *__restrict__ val,
        const double *__restrict__ v, const double *__restrict__ sigc, double *__restrict__ y,
-       double *__restrict__ dpart, Scalars *sc, int cid, int check_done) {
+       double *__restrict__ dpart, Scalars *sc, int cid, int check_done, int keep) {
     __shared__ double red[kBlock / 32];
     if (check_done && sc->done) return;
     if (MODE == 1) TL_BEGIN(sc, 0);
@@ -760,7 +760,13 @@ k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const
     for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
         const int64_t s = rp[i], e = rp[i + 1];
         double a = 0.0;
-        for (int64_t k = s + lane; k < e; k += 32) a = fma(__ldg(val + k), __ldg(v + __ldg(col + k)), a);
+        if (MODE == 1 && keep) {
+            const uint64_t pol = keep_policy();
+            for (int64_t k = s + lane; k < e; k += 32)
+                a = fma(ld_keep(val + k, pol), __ldg(v + ld_keep(col + k, pol)), a);
+        } else {
+            for (int64_t k = s + lane; k < e; k += 32) a = fma(__ldg(val + k), __ldg(v + __ldg(col + k)), a);
+        }
         a = warp_sum(a);
         if (lane == 0) {
             if (MODE == 1) {
@@ -792,14 +798,25 @@ static int grid_for(int64_t units, int per_block) {
     return (int)g;
 }
 
+// PCG-mode SpMV / SpMV^T keep A and A^T in L2 (evict_last loads); IPM_SPMV_KEEP=0 disables
+int spmv_keep() {
+    static int k = -1;
+    if (k < 0) {
+        const char *e = getenv("IPM_SPMV_KEEP");
+        k = e ? atoi(e) : 1;
+    }
+    return k;
+}
+
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
                  Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid, int block) {
     if (P.m == 0) return;
     const int grid = std::min(grid_for(P.m, block / 32), max_grid);
     if (mode == 1)
-        k_spmv<1><<<grid, block, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV_PCG, check_done);
+        k_spmv<1><<<grid, block, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV_PCG, check_done,
+                                          spmv_keep());
     else
-        k_spmv<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV, check_done);
+        k_spmv<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV, check_done, 0);
 }
 
 // ------------------------------------------------ doubly augmented operator, SpMV stage (NEXT-2)

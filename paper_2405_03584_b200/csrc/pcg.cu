@@ -563,7 +563,7 @@ void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
 template <int G>
 __global__ void __launch_bounds__(kBlock)
 k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, const double *__restrict__ ATval,
-        const double *__restrict__ t, double *__restrict__ out, Scalars *sc) {
+        const double *__restrict__ t, double *__restrict__ out, Scalars *sc, int keep) {
     if (sc->done) return;
     TL_BEGIN(sc, 1);
     const int gl = threadIdx.x & (G - 1);
@@ -574,7 +574,13 @@ k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, 
         const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;
         double s = 0.0;
         const int64_t e = ATrp[i + 1];
-        for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
+        if (keep) {
+            const uint64_t pol = keep_policy();
+            for (int64_t k = ATrp[i] + gl; k < e; k += G)
+                s = fma(ld_keep(ATval + k, pol), __ldg(t + ld_keep(ATcol + k, pol)), s);
+        } else {
+            for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
+        }
         s = group_sum<G>(s);
         if (act && gl == 0) out[i] = s;
     }
@@ -586,10 +592,10 @@ static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaS
     if (P.m == 0 || P.n == 0) return;
     const int g = std::min(grid_for(P.n, block / G), max_grid);
     switch (G) {
-        case 4: k_spmvT<4><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
-        case 8: k_spmvT<8><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
-        case 16: k_spmvT<16><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
-        default: k_spmvT<32><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc); break;
+        case 4: k_spmvT<4><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
+        case 8: k_spmvT<8><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
+        case 16: k_spmvT<16><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
+        default: k_spmvT<32><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
     }
 }
 

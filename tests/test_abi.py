@@ -134,7 +134,7 @@ def _sym_plan(lib, n, P, r, grid):
 
 
 @pytest.mark.parametrize("n,P,grid", [(1000, 1, 148), (1000, 2, 148), (1000, 3, 7), (1000, 4, 148), (777, 5, 31),
-                                      (300, 8, 148), (2600, 6, 148), (20000, 1, 148)])
+                                      (300, 8, 148), (2600, 6, 148), (20000, 1, 148), (100000, 8, 148)])
 def test_sym_plan_uses_every_entry_once(lib, n, P, grid):
     """Host-side work plan of the (sharded) symmetric GEMV (NEXT-3 + SURVEY §8(e)): across all
     ranks, every ORDERED entry (i, j) of H enters y = H p exactly once — as a row part of a tile
