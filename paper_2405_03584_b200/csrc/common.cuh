@@ -171,6 +171,37 @@ __device__ __forceinline__ double sum_partials(const double *part, int cnt, doub
     return block_sum(v, sh);
 }
 
+// Two fixed-order sums in one pass (one round of loads, one block reduction): bitwise equal to
+// two sum_partials calls (same per-thread order, same shuffle tree, same warp order).
+// sh2 holds 2 * (blockDim.x / 32) doubles.
+__device__ __forceinline__ void sum_partials2(const double *p, const double *q, int cnt, double *sh2, double &a,
+                                              double &b) {
+    double u = 0.0, v = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        u += ((volatile const double *)p)[i];
+        v += ((volatile const double *)q)[i];
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        u += __shfl_xor_sync(0xffffffffu, u, o);
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    __syncthreads();
+    if (lane == 0) {
+        sh2[wid] = u;
+        sh2[nw + wid] = v;
+    }
+    __syncthreads();
+    double x = 0.0, y = 0.0;
+    for (int i = 0; i < nw; ++i) {
+        x += sh2[i];
+        y += sh2[nw + i];
+    }
+    a = x;
+    b = y;
+}
+
 __device__ __forceinline__ double min_partials(const double *part, int cnt, double *sh) {
     double v = INFINITY;
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) v = fmin(v, ((volatile const double *)part)[i]);

@@ -397,18 +397,36 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
 #ifdef IPM_TIMELINE
     if ((threadIdx.x & 31) == 0) atomicMax(&sc->tl_u[1], gtimer_ns());
 #endif
-    const double a = block_sum(rz, red);
-    const double b = block_sum(rr, red);
-    if (threadIdx.x == 0) {
-        p1[blockIdx.x] = a;
-        p2[blockIdx.x] = b;
+    __shared__ double red2[2 * (BS / 32)];
+    {   // the two block sums in one reduction (bitwise equal to two block_sum calls)
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        double u = rz, v = rr;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            u += __shfl_xor_sync(0xffffffffu, u, o);
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+        }
+        if (lane == 0) {
+            red2[wid] = u;
+            red2[BS / 32 + wid] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = 0.0, b = 0.0;
+            for (int i = 0; i < BS / 32; ++i) {
+                a += red2[i];
+                b += red2[BS / 32 + i];
+            }
+            p1[blockIdx.x] = a;
+            p2[blockIdx.x] = b;
+        }
     }
 #ifdef IPM_TIMELINE
     if (threadIdx.x == 0) atomicMax(&sc->tl_u[2], gtimer_ns());
 #endif
     grid_barrier(&sc->counters[C_BAR], &sc->counters[C_BAR_GEN]);
-    const double trz = sum_partials(p1, gridDim.x, red);
-    const double trr = sum_partials(p2, gridDim.x, red);
+    double trz, trr;
+    sum_partials2(p1, p2, gridDim.x, red2, trz, trr);
     int stop = (trr <= tol2 || it1 >= maxit) ? 1 : 0;
     if (!finite_d(trr) || !finite_d(trz)) stop = 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
