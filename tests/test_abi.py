@@ -179,3 +179,21 @@ def test_sym_plan_uses_every_entry_once(lib, n, P, grid):
         assert used.min() == 1 and used.max() == 1
     # balanced: every rank streams about n^2 / (2P) entries
     assert max(per_rank) <= 1.15 * n * n / (2 * P) + 256 * 256 * 4
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the CPU oracle arm) prints one JSON line with the contract's
+    keys; runs on CPU (workload C1 keeps it to seconds)."""
+    import json
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "C1",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "steps", "warmup", "ms_per_step", "higher_is_better", "cpu_baseline",
+              "e2e", "config"):
+        assert k in d
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["workload"] == "C1"
