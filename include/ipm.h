@@ -110,7 +110,10 @@ typedef struct {
      * comm_handle_host -> ncclUniqueId (128 bytes, from ipm_nccl_unique_id on rank 0,
      * broadcast by the caller); 2 = in-process group, comm_handle_host = ipm_group* (one host
      * thread per rank must drive its context).  comm_kind 2 with nranks 1 runs the sharded
-     * code path on one context (testing). */
+     * code path on one context (testing).  ipm_create is COLLECTIVE when sharded: all ranks
+     * must call it concurrently (communicator setup and the exchange of the H-symmetry
+     * certificate that selects the sharded symmetric GEMV for an exactly symmetric H with an
+     * even chunk; every rank takes the same decision). */
     int64_t row_begin, row_end;
     int32_t rank, nranks;
     int32_t comm_kind;
