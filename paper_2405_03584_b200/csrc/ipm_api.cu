@@ -971,9 +971,9 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         P.gemv_sym = sym ? 1 : 0;
         P.sym_keep = 0;
         if (sym) {
-            // an upper block triangle that fits in L2 (C2: 100 MB of 126 MB) is loaded with an
-            // evict_last policy so it stays resident across PCG iterations; larger H streams
-            // evict_first (measured: no gain from a resident share at C3, -8% GEMV time at C2)
+            // an upper block triangle of <= 100 MiB is loaded with an evict_last policy so it stays
+            // resident across PCG iterations; larger H streams evict_first (measured: no gain from a
+            // resident share at C3; C2's 105 MB forced resident: SYMV -2 % but QP +3 %)
             const double tri = 4.0 * (double)p->n * (double)(p->n + kSymB);
             const char *e = getenv("IPM_SYM_KEEP_MB");      // experiment override
             const double mb = e ? atof(e) : (tri <= 100.0 * 1048576.0 ? 1e9 : 0.0);
