@@ -374,7 +374,8 @@ def run_ours(args):
                          "isolated_launch_ms": gemv_iso_ms,
                          "timing": ("live: in-kernel %globaltimer (first CTA start to last CTA end) summed over "
                                     "every launch in the timed region, on the library stream"
-                                    if kt_n > 0 else "CUDA events, back-to-back launches after the timed region")},
+                                    if kt_n > 0 else "CUDA events, back-to-back launches after the timed region (small n: the timed "
+                                    "PCG ran in the single-CTA k_pcg_small, not in this kernel)")},
             "cpu_baseline": cpu,
             "e2e": {"value": (1 if sharded else ws) * args.steps / float(te.item()), "unit": "QP/s",
                     "h2d_bytes_per_step": int(h2d),
