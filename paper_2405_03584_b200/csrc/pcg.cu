@@ -484,44 +484,88 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
 // iteration for ~1 us of work), so the whole PCG loop runs inside ONE 512-thread CTA:
 // phases separated by __syncthreads, all reductions fixed-order block reductions.  Same
 // recurrence, same stopping rule and scalars as the multi-kernel path.
-__global__ void __launch_bounds__(512)
+// Every vector of the recurrence (and H when it fits) lives in shared memory for the whole
+// loop, so a phase costs shared-memory latency instead of an L2 round trip; the arithmetic and
+// its association are unchanged (bitwise the former global-memory kernel).  A (CSR), sig_c
+// and, when it does not fit, H stay in global memory (read-only, L1-cached).
+constexpr int kSmallThreads = 512;
+constexpr size_t kSmallSmemMax = 200 * 1024;
+
+__device__ __forceinline__ void block_sum2(double &a, double &b, double *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    __syncthreads();
+    if (lane == 0) {
+        sh[wid] = a;
+        sh[32 + wid] = b;
+    }
+    __syncthreads();
+    double ta = 0.0, tb = 0.0;
+    for (int i = 0; i < nw; ++i) {            // fixed order, every thread (block_sum's association)
+        ta += sh[i];
+        tb += sh[32 + i];
+    }
+    a = ta;
+    b = tb;
+}
+
+__global__ void __launch_bounds__(kSmallThreads)
 k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_t *__restrict__ Arp,
             const int *__restrict__ Acol, const double *__restrict__ Aval, const int64_t *__restrict__ ATrp,
             const int *__restrict__ ATcol, const double *__restrict__ ATval, const double *__restrict__ sigb,
             const double *__restrict__ sigc, const double *__restrict__ Minv, double *x, double *r, double *z,
-            double *p, double *t, double *y, Scalars *sc) {
-    __shared__ double red[32];
+            double *p, double *t, double *y, Scalars *sc, int t_in_smem, int h_in_smem) {
+    __shared__ double red[64];
+    extern __shared__ __align__(16) double sm[];
     if (sc->done) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    double *sp = sm, *sr = sm + n, *sz = sm + 2 * n, *sx = sm + 3 * n, *sy = sm + 4 * n, *sM = sm + 5 * n,
+           *sb = sm + 6 * n;
+    double *st = t_in_smem ? sm + 7 * n : t;
+    double *sH = sm + 7 * n + (t_in_smem ? m : 0);
+    const double *Hs = h_in_smem ? sH : H;
+    const int64_t ldhs = h_in_smem ? n : ldh;
+    for (int i = tid; i < n; i += blockDim.x) {
+        sp[i] = p[i];
+        sr[i] = r[i];
+        sz[i] = z[i];
+        sx[i] = x[i];
+        sM[i] = Minv[i];
+        sb[i] = sigb[i];
+    }
+    if (h_in_smem)
+        for (int64_t e = tid; e < (int64_t)n * n; e += blockDim.x) sH[e] = H[(e / n) * ldh + e % n];
     double rho = sc->rho, rho_old = sc->rho_old, rr = sc->rr, pkp = 0.0;
     int64_t it = sc->it, it_rs = sc->it_rs;
     const double tol2 = sc->tol2;
     const int64_t maxit = sc->maxit;
     int breakdown = 0;
+    __syncthreads();
     for (;;) {
         const bool first = (it_rs == 0);
         const double beta = first ? 0.0 : rho / rho_old;
-        for (int i = tid; i < n; i += blockDim.x) p[i] = first ? z[i] : fma(beta, p[i], z[i]);
+        for (int i = tid; i < n; i += blockDim.x) sp[i] = first ? sz[i] : fma(beta, sp[i], sz[i]);
         __syncthreads();
         for (int i = warp; i < m; i += nw) {                      // t = sig_c o (A p)
             double a = 0.0;
-            for (int64_t k = Arp[i] + lane; k < Arp[i + 1]; k += 32) a = fma(Aval[k], p[Acol[k]], a);
+            for (int64_t k = Arp[i] + lane; k < Arp[i + 1]; k += 32) a = fma(Aval[k], sp[Acol[k]], a);
             a = warp_sum(a);
-            if (lane == 0) t[i] = sigc[i] * a;
+            if (lane == 0) st[i] = sigc[i] * a;
         }
         __syncthreads();
         double part = 0.0;
         for (int i = warp; i < n; i += nw) {                      // y = H p + sig_b p + A^T t
             double a = 0.0;
-            const double *h = H + (int64_t)i * ldh;
-            for (int j = lane; j < n; j += 32) a = fma(h[j], p[j], a);
+            const double *h = Hs + (int64_t)i * ldhs;
+            for (int j = lane; j < n; j += 32) a = fma(h[j], sp[j], a);
             if (m > 0)
-                for (int64_t k = ATrp[i] + lane; k < ATrp[i + 1]; k += 32) a = fma(ATval[k], t[ATcol[k]], a);
+                for (int64_t k = ATrp[i] + lane; k < ATrp[i + 1]; k += 32) a = fma(ATval[k], st[ATcol[k]], a);
             a = warp_sum(a);
             if (lane == 0) {
-                const double yi = fma(sigb[i], p[i], a);
-                y[i] = yi;
-                part = fma(p[i], yi, part);
+                const double yi = fma(sb[i], sp[i], a);
+                sy[i] = yi;
+                part = fma(sp[i], yi, part);
             }
         }
         pkp = block_sum(part, red);
@@ -532,16 +576,15 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
         const double alpha = rho / pkp;
         double rz = 0.0, r2 = 0.0;
         for (int i = tid; i < n; i += blockDim.x) {
-            x[i] = fma(alpha, p[i], x[i]);
-            const double ri = fma(-alpha, y[i], r[i]);
-            r[i] = ri;
-            const double zi = Minv[i] * ri;
-            z[i] = zi;
+            sx[i] = fma(alpha, sp[i], sx[i]);
+            const double ri = fma(-alpha, sy[i], sr[i]);
+            sr[i] = ri;
+            const double zi = sM[i] * ri;
+            sz[i] = zi;
             rz = fma(ri, zi, rz);
             r2 = fma(ri, ri, r2);
         }
-        rz = block_sum(rz, red);
-        r2 = block_sum(r2, red);
+        block_sum2(rz, r2, red);
         rho_old = rho;
         rho = rz;
         rr = r2;
@@ -553,6 +596,16 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
         }
         if (rr <= tol2 || it >= maxit) break;
     }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+        p[i] = sp[i];
+        r[i] = sr[i];
+        z[i] = sz[i];
+        x[i] = sx[i];
+        y[i] = sy[i];
+    }
+    if (t_in_smem)
+        for (int i = tid; i < m; i += blockDim.x) t[i] = st[i];
     if (tid == 0) {
         sc->rho = rho;
         sc->rho_old = rho_old;
@@ -566,8 +619,19 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
 }
 
 void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cudaStream_t st) {
-    k_pcg_small<<<1, 512, 0, st>>>(P.n, P.m, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol, P.ATval, V.sig_b,
-                                    V.sig_c, V.Minv, x, V.pr, V.pz, V.pp, V.pt, V.py, sc);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pcg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
+        attr = true;
+    }
+    size_t bytes = 7 * (size_t)P.n * 8;
+    const int t_in = (bytes + (size_t)P.m * 8 <= kSmallSmemMax) ? 1 : 0;
+    if (t_in) bytes += (size_t)P.m * 8;
+    const int h_in = (bytes + (size_t)P.n * P.n * 8 <= kSmallSmemMax) ? 1 : 0;
+    if (h_in) bytes += (size_t)P.n * P.n * 8;
+    k_pcg_small<<<1, kSmallThreads, bytes, st>>>(P.n, P.m, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol,
+                                                 P.ATval, V.sig_b, V.sig_c, V.Minv, x, V.pr, V.pz, V.pp, V.pt, V.py,
+                                                 sc, t_in, h_in);
 }
 
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
