@@ -76,14 +76,19 @@ typedef struct {
     int32_t trace;              /* 1: record one ipm_trace_rec per IPM iteration */
     int32_t use_graph;          /* 1: PCG loop as a CUDA graph with a device-side WHILE node */
     double warm_shift;          /* 1e-3   theta of the warm-start rule (R15) */
-    int32_t gemv_kernel;        /* 0 auto (3 when H == H^T bitwise and unsharded, else 2), 1 LDG.128 register
-                                   tiles, 2 TMA-bulk mbarrier pipeline, 3 symmetric upper-triangle TMA-bulk */
+    int32_t gemv_kernel;        /* 0 auto: 3 when H == H^T bitwise — unsharded by a device compare at create,
+                                   row-sharded by the allgathered hash certificate, and then only with an
+                                   even chunk = ceil(n / nranks) — else 2.  1 LDG.128 register tiles,
+                                   2 TMA-bulk mbarrier pipeline, 3 symmetric upper-triangle TMA-bulk */
     int32_t pcg_warm_start;     /* 0: each PCG starts from x0 = 0 (default, R11); 1: from the previous
                                    search direction (S:248 option) */
     int32_t pcg_system;         /* 0: PCG on the condensed system K dx = rhs (D1, default);
                                    1: PCG on the doubly augmented system eq:2x2_augmented,
                                    unknowns (dx, dlam_lA, dlam_uA), Jacobi preconditioner on its diagonal;
                                    unsharded only, and ipm_pcg() is then rejected (IPM_ERR_STATE) */
+    int32_t kernel_timer;       /* 0 (default): off.  1: the PCG operator kernel (GEMV / SYMV, PCG mode)
+                                   times its own launches on the device for ipm_kernel_timer (two
+                                   atomics per CTA per launch; used by bench.py's live roofline) */
 } ipm_options;
 
 /* Problem description for ipm_create.  Large arrays are BORROWED (the caller keeps them
@@ -257,6 +262,7 @@ int64_t ipm_kernel_launches(const ipm_ctx *ctx);
 /* Live device-side timing of the PCG operator kernel (the dominant GEMV / SYMV in PCG
  * mode): cumulative duration in ms (first CTA start to last CTA end, %globaltimer) and
  * number of timed launches since create, read on ctx's stream (synchronises it).
+ * Counts only with opt.kernel_timer = 1 (else both stay 0).
  * bench.py differences two reads around its timed region.  Host pointers. */
 ipm_status ipm_kernel_timer(ipm_ctx *ctx, double *ms_total_host, int64_t *launches_host);
 

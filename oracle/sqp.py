@@ -162,10 +162,16 @@ def sqp_solve(f: Callable, grad: Callable, h0: np.ndarray, A, l, u, xl, xu, x0,
         t = 1.0
         ft = f(x + d)
         nb = 0
-        while ft > fx + opt.armijo_c1 * t * gd and nb < opt.max_backtrack:
+        while not (ft <= fx + opt.armijo_c1 * t * gd) and nb < opt.max_backtrack:
             t *= 0.5
             ft = f(x + t * d)
             nb += 1
+        if not (ft <= fx + opt.armijo_c1 * t * gd):
+            # no sufficient decrease (or a non-finite trial value): the step is not taken, since
+            # the merit function must be nonincreasing across accepted steps
+            trace.append(dict(rec, step=0.0, theta=1.0, updated=False))
+            status = "line_search_failed"
+            break
         s = t * d
         x = x + s
         g_new = grad(x)

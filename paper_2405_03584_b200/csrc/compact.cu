@@ -19,7 +19,7 @@
 
 namespace ipm {
 
-constexpr int kCompactThreads = 256;   // >= k (columns) — checked at create (k <= 256 per pass slice)
+constexpr int kCompactThreads = 256;   // warp-per-row CTAs of k_compact_us; ldu <= kCompactMaxCols checked at create
 
 constexpr int kUtThreads = 1024;       // 4 row groups x 256 column slots
 constexpr int kUtGroups = kUtThreads / 256;

@@ -750,6 +750,10 @@ IPM_EXPORT ipm_status ipm_workspace_size(const ipm_problem *p, const ipm_options
     Layout L;
     if (p->hess_kind == 1 && (p->ldu < 1 || p->k < 0 || p->k > p->ldu))
         return fail(nullptr, IPM_ERR_INVALID, "compact Hessian needs 0 <= k <= ldu and ldu >= 1");
+    // k_compact_us stages w o s (k doubles, k <= ldu) in its 48 KB default dynamic shared memory
+    if (p->hess_kind == 1 && p->ldu > kCompactMaxCols)
+        return fail(nullptr, IPM_ERR_INVALID, "compact Hessian: ldu = %lld exceeds %d columns", (long long)p->ldu,
+                    kCompactMaxCols);
     plan(nloc, p->n, p->m, p->nnz, eff_ranks(p), L, p->hess_kind == 1 ? p->ldu : 0, p->rank);   // local A^T nnz <= nnz
     *bytes = L.total;
     return IPM_OK;
@@ -1012,14 +1016,15 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         if (ctx->opt.pcg_system == 1 && ctx->sharded)
             return fail(ctx, IPM_ERR_INVALID, "pcg_system = 1 (doubly augmented) is unsharded only");
         P.aug = (ctx->opt.pcg_system == 1 && p->m > 0) ? 1 : 0;
+        P.ktimer = ctx->opt.kernel_timer ? 1 : 0;
         ctx->G = choose_group(p->nnz, nloc, ctx->ncb);
-        {
-            static bool carve = false;
+        {   // function attributes are per device: set them for this context's device on every create
+            CK(configure_linalg_attrs());
+            CK(configure_pcg_attrs());
             const char *ce = getenv("IPM_CARVEOUT");
-            if (!carve && !(ce && atoi(ce) == 0)) {
+            if (!(ce && atoi(ce) == 0)) {
                 configure_linalg_carveout();
                 configure_pcg_carveout();
-                carve = true;
             }
         }
         {   // fused update + p (cooperative grid barrier): single-GPU condensed PCG

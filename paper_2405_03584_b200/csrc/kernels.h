@@ -84,6 +84,8 @@ void launch_sym_hash(int nloc, int ncols, int64_t row_begin, int chunk, int nran
 int side_block();
 int spmv_keep();    // 1: PCG-mode SpMV / SpMV^T load A, A^T with an L2 evict_last priority   // CTA size of every PCG-mode SpMV launch (one association => bitwise paths)
 void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
+cudaError_t configure_linalg_attrs();   // >48 KB dynamic smem opt-ins (per device: called at every create)
+cudaError_t configure_pcg_attrs();
 void configure_pcg_carveout();
 // NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,
 // yu = -A px + D_u pu (masked); mode 1 (PCG): done check + S_c = a.t + pl.yl + pu.yu
@@ -103,6 +105,7 @@ void launch_rank2(const Prob &P, int row0, const double *u, double a, const doub
 
 // compact.cu (NEXT-1: H = diag(h0) + U diag(w) U^T, matrix-free)
 constexpr int kCompactGrid = 148;   // U^T p: one 1024-thread CTA per SM
+constexpr int kCompactMaxCols = 6144;   // w o s staged in 48 KB of dynamic smem (k_compact_us)
 void launch_compact_apply(const Prob &P, const double *v, const double *vdot, double *ypart, Scalars *sc, int mode,
                           int cid, cudaStream_t st);
 void launch_compact_diag(const Prob &P, cudaStream_t st);

@@ -38,11 +38,11 @@ template <bool VEC, int MODE>
 __global__ void __launch_bounds__(kGemvThreads)
 k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
              const double *__restrict__ p, const double *__restrict__ pdot,
-             double *__restrict__ ypart, int ncb, double *__restrict__ dpart, Scalars *sc, int cid) {
+             double *__restrict__ ypart, int ncb, double *__restrict__ dpart, Scalars *sc, int cid, int timed) {
     __shared__ __align__(16) double ps[kGemvCW];
     __shared__ double red[kGemvThreads / 32];
     if (MODE == 1 && sc->done) return;
-    if (MODE == 1) ktimer_start(&sc->kt_neg);
+    if (MODE == 1 && timed) ktimer_start(&sc->kt_neg);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nrb = (nrows + kGemvRB - 1) / kGemvRB;
     const int64_t ntiles = (int64_t)nrb * ncb;
@@ -117,7 +117,7 @@ k_gemv_tiles(const double *__restrict__ H, int64_t ldh, int nrows, int ncols,
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
-            if (MODE == 1) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
+            if (MODE == 1 && timed) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
             if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
             // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
@@ -141,11 +141,11 @@ void launch_gemv(const Prob &P, const double *v, const double *vdot, double *ypa
         return;
     }
     if (mode == 1) {
-        if (vec) k_gemv_tiles<true, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
-        else k_gemv_tiles<false, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+        if (vec) k_gemv_tiles<true, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid, P.ktimer);
+        else k_gemv_tiles<false, 1><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid, P.ktimer);
     } else {
-        if (vec) k_gemv_tiles<true, 0><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
-        else k_gemv_tiles<false, 0><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+        if (vec) k_gemv_tiles<true, 0><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid, P.ktimer);
+        else k_gemv_tiles<false, 0><<<grid, kGemvThreads, 0, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid, P.ktimer);
     }
 }
 
@@ -209,11 +209,11 @@ template <int MODE>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 k_gemv_bulk(const double *__restrict__ H, int64_t ldh, int nrows, int ncols, const double *__restrict__ p,
             const double *__restrict__ pdot, double *__restrict__ ypart, int ncb, double *__restrict__ dpart,
-            Scalars *sc, int cid) {
+            Scalars *sc, int cid, int timed) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[kBulkThreads / 32];
     if (MODE == 1 && sc->done) return;
-    if (MODE == 1) ktimer_start(&sc->kt_neg);
+    if (MODE == 1 && timed) ktimer_start(&sc->kt_neg);
     double *stages = reinterpret_cast<double *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kBulkStages * kBulkStageDoubles * 8);
     uint64_t *empty = full + kBulkStages;
@@ -299,7 +299,7 @@ k_gemv_bulk(const double *__restrict__ H, int64_t ldh, int nrows, int ncols, con
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
-            if (MODE == 1) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
+            if (MODE == 1 && timed) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
             if (sc->sharded) sc->loc[1] = tot;      // local p^T H_loc p; alpha via k_xcombine
             // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
@@ -310,26 +310,16 @@ bool gemv_bulk_ok(const Prob &P) {
     return ((P.ldh & 1) == 0) && ((reinterpret_cast<uintptr_t>(P.H) & 15) == 0);
 }
 
-int gemv_bulk_grid() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_gemv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
-        cudaFuncSetAttribute(k_gemv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
-    }
-    return sms;
-}
+int gemv_bulk_grid() { return num_sms(); }
 
 // v must be 16-byte aligned and readable up to round_up(ncols, 2) doubles (workspace vectors).
 void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, int ncb, double *dpart,
                       Scalars *sc, int grid, int mode, int cid, cudaStream_t st) {
     if (P.n == 0) return;
     if (mode == 1)
-        k_gemv_bulk<1><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+        k_gemv_bulk<1><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid, P.ktimer);
     else
-        k_gemv_bulk<0><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid);
+        k_gemv_bulk<0><<<grid, kBulkThreads, kBulkSmem, st>>>(P.H, P.ldh, P.n, P.ncols, v, vdot, ypart, ncb, dpart, sc, cid, P.ktimer);
 }
 
 // ------------------------------------------------------- symmetric GEMV (upper block triangle)
@@ -396,12 +386,12 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
             const SymRange *__restrict__ ranges, const double *__restrict__ p, int64_t row_begin,
             const double *__restrict__ pdot, double *__restrict__ ypart, int ldy, int ycarry,
             double *__restrict__ zpart, int ldz, int zcarry, double *__restrict__ dpart, Scalars *sc, int cid,
-            int keep, const double *__restrict__ sigb_dot) {
+            int keep, const double *__restrict__ sigb_dot, int timed) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[kSymThreads / 32];
     __shared__ double colbuf[kSymB];                  // row-half-1 column sums of the current tile
     if (MODE == 1 && sc->done) return;
-    if (MODE == 1) ktimer_start(&sc->kt_neg);
+    if (MODE == 1 && timed) ktimer_start(&sc->kt_neg);
     if (MODE == 1) TL_BEGIN(sc, 2);
     double *stages = reinterpret_cast<double *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kSymStages * kSymStageDoubles * 8);
@@ -561,7 +551,7 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
             sc->S_H = tot;
-            if (MODE == 1) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
+            if (MODE == 1 && timed) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
             if (sc->sharded) sc->loc[1] = tot;
             // alpha = rho / (S_H + S_b + S_c) is formed by k_pcg_update (the SpMV runs concurrently)
         }
@@ -571,21 +561,15 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
 
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
                       int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_symv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
-        cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
-        attr = true;
-    }
     const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(P.tmap_sym);
     if (mode == 1)
         k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
                                                              P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
-                                                             dpart, sc, cid, P.sym_keep, sigb_dot);
+                                                             dpart, sc, cid, P.sym_keep, sigb_dot, P.ktimer);
     else
         k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
                                                              P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
-                                                             dpart, sc, cid, P.sym_keep, sigb_dot);
+                                                             dpart, sc, cid, P.sym_keep, sigb_dot, P.ktimer);
 }
 
 // Work plan of the symmetric GEMV (kernels.h).  Blocks: every rank's rows cut into kSymB
@@ -1141,6 +1125,17 @@ void launch_rank2(const Prob &P, int row0, const double *u, double a, const doub
 // max-shared L1/smem carveout: otherwise an SM holding a GEMV CTA is not eligible for their
 // CTAs (different carveout) and the SpMV side branch waits for the GEMV to drain (measured:
 // the side branch started 215 us into a 240 us GEMV, scripts/timeline_probe.py).
+// Dynamic shared-memory opt-ins of the >48 KB kernels.  Function attributes are per device
+// (per primary context), so ipm_create calls this for the context's device every time.
+cudaError_t configure_linalg_attrs() {
+    cudaError_t e = cudaSuccess, r;
+    if ((r = cudaFuncSetAttribute(k_gemv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem))) e = r;
+    if ((r = cudaFuncSetAttribute(k_gemv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem))) e = r;
+    if ((r = cudaFuncSetAttribute(k_symv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem))) e = r;
+    if ((r = cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem))) e = r;
+    return e;
+}
+
 void configure_linalg_carveout() {
     const int c = cudaSharedmemCarveoutMaxShared;
     cudaFuncSetAttribute(k_spmv<0>, cudaFuncAttributePreferredSharedMemoryCarveout, c);

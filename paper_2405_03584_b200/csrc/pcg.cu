@@ -618,12 +618,11 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
     }
 }
 
+cudaError_t configure_pcg_attrs() {
+    return cudaFuncSetAttribute(k_pcg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
+}
+
 void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pcg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
-        attr = true;
-    }
     size_t bytes = 7 * (size_t)P.n * 8;
     const int t_in = (bytes + (size_t)P.m * 8 <= kSmallSmemMax) ? 1 : 0;
     if (t_in) bytes += (size_t)P.m * 8;

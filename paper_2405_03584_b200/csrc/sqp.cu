@@ -424,7 +424,8 @@ ipm_status solve_impl(ipm_sqp *S, const double *x0) {
         launch_f(S, S->x, S->d, t, 0);
         if (sync(S) != IPM_OK) return IPM_ERR_CUDA;
         ft = S->hsc->red[0];
-        while (ft > f + o.armijo_c1 * t * gd && nb < o.max_backtrack) {
+        // written as !(ft <= ...) so a NaN trial value keeps backtracking instead of being accepted
+        while (!(ft <= f + o.armijo_c1 * t * gd) && nb < o.max_backtrack) {
             t *= 0.5;
             ++nb;
             launch_f(S, S->x, S->d, t, 0);
@@ -432,6 +433,15 @@ ipm_status solve_impl(ipm_sqp *S, const double *x0) {
             ft = S->hsc->red[0];
         }
         st.backtracks += nb;
+        if (!(ft <= f + o.armijo_c1 * t * gd)) {
+            // no sufficient decrease within max_backtrack halvings: the step is NOT taken (the
+            // merit function must not increase across accepted steps)
+            status = std::isfinite(ft) ? IPM_NOT_CONVERGED : IPM_ERR_NONFINITE;
+            sfail(S, status, "line search failed at SQP iteration %d (f(x + t d) = %g after %d halvings)", k, ft, nb);
+            rec.step = 0.0;
+            S->trace.push_back(rec);
+            break;
+        }
         // x_{k+1} = x + t d (same fma as the trial), s = t d; gradient at x_{k+1}
         launch_vec(S, V_STEP, S->d, S->x, nullptr, nullptr, t, S->tmp, S->s);
         std::swap(S->x, S->tmp);

@@ -103,6 +103,7 @@ struct Prob {
     double *h0, *w;        // workspace copies (w has capacity ldu)
     double *cs, *cspart, *chpart;   // s = U^T p (ldu), per-CTA column partials, per-CTA h0 p^2 partials
     int aug;               // 1: PCG on the doubly augmented system eq:2x2_augmented
+    int ktimer;            // 1: the PCG-mode operator kernel times its launches (opt.kernel_timer)
 };
 
 // Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).
