@@ -21,7 +21,8 @@ so x* stays the exact optimum of QP k and f*_k = 1/2 x*^T H_k x* + g_k^T x* is k
 earlier version let g drift by 0.05 N(0, 1) per QP; that left the optimum unplanted and nearly
 degenerate, and QP 1 at C3 size took 37 IPM / 4.1 M PCG iterations instead of 18 / 0.2 M.)
 Every update (u, alpha, v, beta, g_k) is handed identically to the GPU path
-(ipm_update_hessian_rank2 / ipm_set_linear_term) and to the oracle (dense numpy update).
+(ipm_update_hessian_rank2 / ipm_set_linear_term) and to the oracle (oracle.bfgs.rank2_update);
+this module only draws them.
 """
 from __future__ import annotations
 
@@ -77,8 +78,3 @@ def sqp_sequence(q, K: int, seed: int = 0, rank_G: int = 32) -> List[Update]:
         out.append(Update(u=u, alpha=alpha, v=y, beta=beta, g=g, f_star=f_star))
     return out
 
-
-def apply_dense(H: np.ndarray, up: Update) -> None:
-    """In-place dense update used by the oracle side (numpy)."""
-    H += up.alpha * np.outer(up.u, up.u)
-    H += up.beta * np.outer(up.v, up.v)

@@ -238,6 +238,18 @@ ipm_status ipm_op_diag(ipm_ctx *ctx, const double *sig_b, const double *sig_c, d
 ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *rhs,
                    double *x, double rtol, int32_t *iters_host);
 
+/* Test hook (PCG-mode operator parity): exactly k >= 1 iterations of the PCG
+ * recurrence ipm_solve runs (Jacobi PCG) on K x = rhs from x0 = 0, with
+ * Sigma_b = sig_b, Sigma_c = sig_c — the same kernels and launch path (single-CTA loop for small
+ * n; otherwise the CUDA graph: symmetric GEMV in PCG mode with p^T (H + Sigma_b) p fused, the
+ * SpMV / SpMV^T branch, the fused cooperative update), but no stopping test, no true-residual
+ * confirmation and no restart.  Outputs (device, this rank's rows; NULL = skip): x_k, r_k,
+ * z_k = M^-1 r_k, and p = the search direction used by iteration k.  scal_host (NULL = skip)
+ * receives 4 doubles {rho_k = r_k^T z_k, p^T K p of iteration k, alpha_k, ||r_k||^2}.
+ * IPM_ERR_PCG_BREAKDOWN if p^T K p <= 0 or a non-finite value occurs. */
+ipm_status ipm_pcg_iterate(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *rhs, int32_t k,
+                           double *x, double *r, double *z, double *p, double *scal_host);
+
 /* Measurement hook (bench.py roofline): launch one hot-path stage `reps` times back to back
  * on the context's stream, bracketed by CUDA events recorded on that stream, with the
  * current PCG vectors as operands; *ms_host = average device time per launch.

@@ -30,7 +30,12 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
     libipm_tl.so; loaded only when IPM_LIB points at it (scripts/timeline_probe.py)."""
     lib = LIB if not variant else LIB.replace("libipm.so", f"libipm_{variant}.so")
     extra = {"tl": ["-DIPM_TIMELINE"], "sr16": ["-DIPM_SYM_SR=16", "-DIPM_SYM_STAGES=6"],
-             "sr16s4": ["-DIPM_SYM_SR=16", "-DIPM_SYM_STAGES=4"]}.get(variant, [])
+             "sr16s4": ["-DIPM_SYM_SR=16", "-DIPM_SYM_STAGES=4"],
+             "nc": ["-DIPM_SYM_NOCOMPUTE"], "nocol": ["-DIPM_SYM_NOCOL"],
+             "pf1": ["-DIPM_SYM_PF=1"], "pf2": ["-DIPM_SYM_PF=2"], "pf3": ["-DIPM_SYM_PF=3"],
+             "pf4": ["-DIPM_SYM_PF=4"], "pf6": ["-DIPM_SYM_PF=6"], "pf3nc": ["-DIPM_SYM_PF=3", "-DIPM_SYM_NOCOMPUTE"],
+             "lds4": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=4"], "lds2": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=2"],
+             "lds6": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=6"], "lds4nc": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_NOCOMPUTE"]}.get(variant, [])
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers += [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
     objdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))

@@ -380,17 +380,25 @@ struct PcgOut {
 };
 
 // Solve K dx = rhs (V.rhs -> V.dx) with the current diagonals; Minv already set.
-ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
+// fixed > 0 (test hook ipm_pcg_iterate): exactly `fixed` iterations from x0 = 0 — no stopping
+// test (tolerance 0), no true-residual confirmation, no restart; same kernels and launch path.
+ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) {
     const Prob &P = ctx->P;
     Vecs &V = ctx->V;
     int64_t maxit = ctx->opt.pcg_max_iter > 0 ? ctx->opt.pcg_max_iter : 10 * (int64_t)ctx->n;
+    double atol = ctx->opt.pcg_atol;
+    if (fixed > 0) {
+        maxit = fixed;
+        rtol = 0.0;
+        atol = 0.0;
+    }
     // warm start (option): x0 = the previous direction still held in V.dx
-    const int warm = (ctx->opt.pcg_warm_start && ctx->have_dx) ? 1 : 0;
-    launch_pcg_init(P, V, ctx->sc, V.rhs, V.dx, rtol, ctx->opt.pcg_atol, maxit, warm, ctx->st);
+    const int warm = (fixed == 0 && ctx->opt.pcg_warm_start && ctx->have_dx) ? 1 : 0;
+    launch_pcg_init(P, V, ctx->sc, V.rhs, V.dx, rtol, atol, maxit, warm, ctx->st);
     DSYNC("pcg_init");
     ctx->launches += 1;
     CKL();
-    TRY(xcombine(ctx, X_PCG_INIT, rtol, ctx->opt.pcg_atol, maxit));
+    TRY(xcombine(ctx, X_PCG_INIT, rtol, atol, maxit));
     if (warm) {
         TRY(op_apply(ctx, V.dx, nullptr, V.pr, V.rhs, 1));      // r = rhs - K x0
         launch_pcg_restart(P, V, ctx->sc, ctx->st);              // z, rho, rr, done
@@ -447,6 +455,10 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out) {
             out.iters = h.it;
             return fail(ctx, IPM_ERR_PCG_BREAKDOWN, "PCG breakdown at iteration %lld (p^T K p = %g)",
                         (long long)h.it, h.pKp);
+        }
+        if (fixed > 0) {
+            out.iters = h.it;
+            break;
         }
         // true residual confirmation: r = rhs - K dx
         TRY(op_apply(ctx, V.dx, nullptr, V.pr, V.rhs, 1));
@@ -553,6 +565,8 @@ ipm_status solve_impl(ipm_ctx *ctx) {
     ctx->have_iterate = true;
     TRY(residuals(ctx, ctx->mu));
     TRY(sync_scalars(ctx));
+    // a starting iterate with Inf/NaN entries (ipm_set_iterate) cannot produce a direction
+    if (ctx->hsc->nonfinite) return fail(ctx, IPM_ERR_NONFINITE, "non-finite residual at the starting iterate");
     double mu = ctx->mu;
     float tpcg = 0.f;
     ipm_status status = IPM_NOT_CONVERGED;
@@ -1084,7 +1098,9 @@ IPM_EXPORT ipm_status ipm_create(ipm_ctx **out, const ipm_problem *p, const ipm_
 IPM_EXPORT ipm_status ipm_solve(ipm_ctx *ctx) {
     if (!ctx) return fail(nullptr, IPM_ERR_INVALID, "null context");
     ctx->err.clear();
-    return solve_impl(ctx);
+    const ipm_status s = solve_impl(ctx);
+    if (s != IPM_OK && s != IPM_NOT_CONVERGED) ctx->stats.status = s;   // early error exits
+    return s;
 }
 
 IPM_EXPORT ipm_status ipm_get_solution(ipm_ctx *ctx, double *x, double *lam_lA, double *lam_uA, double *lam_lx,
@@ -1251,6 +1267,32 @@ IPM_EXPORT ipm_status ipm_pcg(ipm_ctx *ctx, const double *sig_b, const double *s
     CK(cudaStreamSynchronize(ctx->st));
     if (iters) *iters = (int32_t)po.iters;
     if (po.stalled) return fail(ctx, IPM_NOT_CONVERGED, "PCG reached its iteration limit (relres %g)", po.relres);
+    return IPM_OK;
+}
+
+IPM_EXPORT ipm_status ipm_pcg_iterate(ipm_ctx *ctx, const double *sig_b, const double *sig_c, const double *rhs,
+                                      int32_t k, double *x, double *r, double *z, double *p, double *scal) {
+    if (!ctx || !sig_b || !rhs || k < 1 || (ctx->m > 0 && !sig_c)) return fail(ctx, IPM_ERR_INVALID, "bad argument");
+    if (ctx->P.aug) return fail(ctx, IPM_ERR_STATE, "ipm_pcg_iterate runs the condensed system: pcg_system = 0");
+    TRY(load_sigmas(ctx, sig_b, sig_c));
+    launch_jacobi(ctx->P, ctx->G, ctx->V.sig_b, ctx->V.sig_c, ctx->V.Minv, 1, ctx->st);
+    CK(cudaMemcpyAsync(ctx->V.rhs, rhs, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToDevice, ctx->st));
+    ctx->launches += 1;
+    PcgOut po;
+    TRY(pcg_solve(ctx, 0.0, po, k));
+    const size_t nb = sizeof(double) * ctx->nloc;
+    if (x) CK(cudaMemcpyAsync(x, ctx->V.dx, nb, cudaMemcpyDeviceToDevice, ctx->st));
+    if (r) CK(cudaMemcpyAsync(r, ctx->V.pr, nb, cudaMemcpyDeviceToDevice, ctx->st));
+    if (z) CK(cudaMemcpyAsync(z, ctx->V.pz, nb, cudaMemcpyDeviceToDevice, ctx->st));
+    if (p) CK(cudaMemcpyAsync(p, ctx->V.pp, nb, cudaMemcpyDeviceToDevice, ctx->st));
+    TRY(sync_scalars(ctx));
+    if (ctx->hsc->it != k) return fail(ctx, IPM_ERR_STATE, "ran %lld PCG iterations, expected %d", (long long)ctx->hsc->it, k);
+    if (scal) {
+        scal[0] = ctx->hsc->rho;
+        scal[1] = ctx->hsc->pKp;
+        scal[2] = ctx->hsc->alpha;
+        scal[3] = ctx->hsc->rr;
+    }
     return IPM_OK;
 }
 

@@ -339,7 +339,17 @@ void launch_gemv_bulk(const Prob &P, const double *v, const double *vdot, double
 #endif
 constexpr int kSymStages = IPM_SYM_STAGES;
 constexpr int kSymConsumers = 16;                 // consumer warps (2 per strip row pair)
-constexpr int kSymThreads = 32 * (kSymConsumers + 1);
+#ifdef IPM_SYM_LDGSTS
+// experiment: the ring is filled by kSymLoaders warps with LSU async copies (cp.async.cg,
+// 16 B per thread, completion via cp.async.mbarrier.arrive.noinc) instead of the TMA unit
+#ifndef IPM_SYM_LOADERS
+#define IPM_SYM_LOADERS 4
+#endif
+constexpr int kSymLoaders = IPM_SYM_LOADERS;
+#else
+constexpr int kSymLoaders = 1;
+#endif
+constexpr int kSymThreads = 32 * (kSymConsumers + kSymLoaders);
 constexpr int kSymRW = kSymSR / kSymConsumers;    // strip rows reduced by each consumer warp
 constexpr int kSymStageDoubles = kSymSR * kSymB + kSymB + kSymSR;
 constexpr size_t kSymSmem = (size_t)kSymStages * kSymStageDoubles * 8 + 2 * kSymStages * 8;
@@ -380,6 +390,35 @@ bool make_sym_tensor_map(const Prob &P, void *out) {
     return r == CUDA_SUCCESS;
 }
 
+#ifdef IPM_SYM_LDGSTS
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t *b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// the loader variant reads H through plain pointers: base, leading dimension and extents are
+// passed in the (unused) tensor-map argument's storage by launch_symv_bulk
+struct SymRaw { const double *H; int64_t ldh; int rows, cols; };
+__device__ __forceinline__ const double *tmap_base(const CUtensorMap *t) { return reinterpret_cast<const SymRaw *>(t)->H; }
+__device__ __forceinline__ int64_t tmap_ld(const CUtensorMap *t) { return reinterpret_cast<const SymRaw *>(t)->ldh; }
+__device__ __forceinline__ int tmap_rows(const CUtensorMap *t) { return reinterpret_cast<const SymRaw *>(t)->rows; }
+__device__ __forceinline__ int tmap_cols(const CUtensorMap *t) { return reinterpret_cast<const SymRaw *>(t)->cols; }
+#endif
+
+// L2 prefetch of a strip (no shared memory, no completion): lets the producer run PF strips
+// ahead of the smem ring, so more bytes are in flight than the ring holds.
+__device__ __forceinline__ void tma_2d_prefetch_l2(const CUtensorMap *tmap, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y)
+                 : "memory");
+}
+#ifndef IPM_SYM_PF
+#define IPM_SYM_PF 0
+#endif
+constexpr int kSymPF = IPM_SYM_PF;     // strips of L2 prefetch distance (0 = off)
+
 template <int MODE>
 __global__ void __launch_bounds__(kSymThreads, 1)
 k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict__ tiles,
@@ -399,7 +438,11 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kSymStages; ++s) {
+#ifdef IPM_SYM_LDGSTS
+            mbar_init(&full[s], 32 * kSymLoaders);
+#else
             mbar_init(&full[s], 1);
+#endif
             mbar_init(&empty[s], kSymConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -408,19 +451,76 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
     const SymRange rg = ranges[blockIdx.x];
     const int tlast = rg.s1 > 0 ? rg.t1 : rg.t1 - 1;     // last tile touched (inclusive)
     double dacc = 0.0;
+#ifdef IPM_SYM_LDGSTS
+    if (warp >= kSymConsumers) {
+        // loader threads: 16-B async copies of the 32 x 256 strip (zero-filled outside H), p_J, p_I
+        const int lt = threadIdx.x - kSymConsumers * 32;
+        constexpr int NL = 32 * kSymLoaders;
+        const double *Hb = tmap_base(&tmap);
+        const int64_t ldh = tmap_ld(&tmap);
+        const int nrows_all = tmap_rows(&tmap), ncols_all = tmap_cols(&tmap);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = rg.t0; t <= tlast; ++t) {
+            const SymTile T = tiles[t];
+            const int sa = (t == rg.t0) ? rg.s0 : 0;
+            const int sb = (t == rg.t1) ? rg.s1 : (T.rows + kSymSR - 1) / kSymSR;
+            for (int sidx = sa; sidx < sb; ++sidx) {
+                const int s0 = sidx * kSymSR;
+                mbar_wait(&empty[stage], phase ^ 1u);
+                double *sH = stages + (size_t)stage * kSymStageDoubles;
+                double *sPJ = sH + kSymSR * kSymB;
+                double *sPI = sPJ + kSymB;
+                // H: kSymSR rows x kSymB cols = kSymSR * kSymB / 2 chunks of 16 B
+                for (int q = lt; q < kSymSR * kSymB / 2; q += NL) {
+                    const int r = q / (kSymB / 2), c2 = (q % (kSymB / 2)) * 2;
+                    const int gr = T.r0 + s0 + r, gc = T.c0 + c2;
+                    const bool ok = gr < nrows_all && gc < ncols_all;
+                    const double *src = ok ? Hb + (int64_t)gr * ldh + gc : Hb;
+                    cp_async16(sH + r * kSymB + c2, src, ok ? 16 : 0);
+                }
+                for (int q = lt; q < kSymB / 2; q += NL) {
+                    const int gc = T.c0 + 2 * q;
+                    const bool ok = gc < ncols_all;
+                    cp_async16(sPJ + 2 * q, ok ? p + gc : p, ok ? 16 : 0);
+                }
+                for (int q = lt; q < kSymSR / 2; q += NL) {
+                    const int64_t gi = row_begin + T.r0 + s0 + 2 * q;
+                    const bool ok = T.r0 + s0 + 2 * q < nrows_all;
+                    cp_async16(sPI + 2 * q, ok ? p + gi : p, ok ? 16 : 0);
+                }
+                cp_async_mbar_arrive_noinc(&full[stage]);
+                if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
+            }
+        }
+    } else if (false) {
+#else
     if (warp == kSymConsumers) {
+#endif
         if (lane == 0) {
             uint64_t pol_h, pol_p;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_h));
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_p));
             int stage = 0;
             uint32_t phase = 0;
+            // prefetch cursor (pt, ps): kSymPF strips ahead of the load cursor, same range
+            int pt = rg.t0, ps = rg.s0, pend = 0;
+            auto pf_next = [&]() {
+                if (pt > tlast) return;
+                const SymTile P2 = tiles[pt];
+                const int pe = (pt == rg.t1) ? rg.s1 : (P2.rows + kSymSR - 1) / kSymSR;
+                if (ps < pe) tma_2d_prefetch_l2(&tmap, P2.c0, P2.r0 + ps * kSymSR);
+                if (++ps >= pe) { ++pt; ps = 0; }
+            };
+            if (kSymPF > 0)
+                for (; pend < kSymPF; ++pend) pf_next();
             for (int t = rg.t0; t <= tlast; ++t) {
                 const SymTile T = tiles[t];
                 const int cwb = (T.cols + 1) & ~1;
                 const int sa = (t == rg.t0) ? rg.s0 : 0;
                 const int sb = (t == rg.t1) ? rg.s1 : (T.rows + kSymSR - 1) / kSymSR;
                 for (int sidx = sa; sidx < sb; ++sidx) {
+                    if (kSymPF > 0) pf_next();
                     const int s0 = sidx * kSymSR;
                     const int rows = min(kSymSR, T.rows - s0);
                     const int rb = (rows + 1) & ~1;
@@ -462,6 +562,13 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
                 const double *sH = stages + (size_t)stage * kSymStageDoubles;
                 const double *sPJ = sH + kSymSR * kSymB;
                 const double *sPI = sPJ + kSymB;
+#ifdef IPM_SYM_NOCOMPUTE
+                // experiment only (build variant "nc"): the pure TMA stream rate of this work plan
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+                if (++stage == kSymStages) { stage = 0; phase ^= 1u; }
+                continue;
+#endif
                 if (sidx == sa && c < colsJ) pj_c = sPJ[c];
                 // row part: rows warp + 16 q (q < kSymRW) of the strip (OOB rows are zero-filled)
                 const double2 *pv = reinterpret_cast<const double2 *>(sPJ);
@@ -510,7 +617,11 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
                     }
                 }
                 // column part (H_IJ^T p_I): this thread's column over its half of the strip rows
+#ifdef IPM_SYM_NOCOL
+                if (false) {
+#else
                 if (!diag && c < colsJ) {
+#endif
                     const int rb0 = h * (kSymSR / 2);
 #pragma unroll
                     for (int r = 0; r < kSymSR / 2; r += 2) {
@@ -561,7 +672,17 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
 
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
                       int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot) {
+#ifdef IPM_SYM_LDGSTS
+    CUtensorMap raw;
+    SymRaw *sr = reinterpret_cast<SymRaw *>(&raw);
+    sr->H = P.H;
+    sr->ldh = P.ldh;
+    sr->rows = P.n;
+    sr->cols = P.ncols;
+    const CUtensorMap &tm = raw;
+#else
     const CUtensorMap &tm = *reinterpret_cast<const CUtensorMap *>(P.tmap_sym);
+#endif
     if (mode == 1)
         k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
                                                              P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,

@@ -536,7 +536,7 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
     }
     if (h_in_smem)
         for (int64_t e = tid; e < (int64_t)n * n; e += blockDim.x) sH[e] = H[(e / n) * ldh + e % n];
-    double rho = sc->rho, rho_old = sc->rho_old, rr = sc->rr, pkp = 0.0;
+    double rho = sc->rho, rho_old = sc->rho_old, rr = sc->rr, pkp = 0.0, alpha_last = 0.0;
     int64_t it = sc->it, it_rs = sc->it_rs;
     const double tol2 = sc->tol2;
     const int64_t maxit = sc->maxit;
@@ -574,6 +574,7 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
             break;
         }
         const double alpha = rho / pkp;
+        alpha_last = alpha;
         double rz = 0.0, r2 = 0.0;
         for (int i = tid; i < n; i += blockDim.x) {
             sx[i] = fma(alpha, sp[i], sx[i]);
@@ -611,6 +612,7 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
         sc->rho_old = rho_old;
         sc->rr = rr;
         sc->pKp = pkp;
+        sc->alpha = alpha_last;
         sc->it = it;
         sc->it_rs = it_rs;
         sc->done = 1;

@@ -260,3 +260,13 @@ class QP:
         st = L.ipm_pcg(self.ctx, _ptr(sb), _ptr(scv), _ptr(r), _ptr(x), float(rtol), C.byref(it))
         L.check(st, self.ctx, allow=(L.IPM_OK, L.IPM_NOT_CONVERGED))
         return x, it.value
+
+    def pcg_iterate(self, sig_b, sig_c, rhs, k: int) -> dict:
+        """Exactly k PCG iterations of the solve's own kernels (ipm_pcg_iterate test hook)."""
+        sb, scv, r = (_dev(a, torch.float64, self.device) for a in (sig_b, sig_c, rhs))
+        out = {key: torch.empty(self.nloc, dtype=torch.float64, device=self.device) for key in ("x", "r", "z", "p")}
+        sc = (C.c_double * 4)()
+        L.check(L.ipm_pcg_iterate(self.ctx, _ptr(sb), _ptr(scv), _ptr(r), int(k), _ptr(out["x"]), _ptr(out["r"]),
+                                  _ptr(out["z"]), _ptr(out["p"]), sc), self.ctx)
+        out.update(rho=sc[0], pKp=sc[1], alpha=sc[2], rr=sc[3])
+        return out

@@ -64,13 +64,14 @@ def test_c4_sequence_stays_planted():
     """after every BFGS rank-2 update of H the planted formula re-derives g_k,
     so the planted x* is the exact optimum of each QP of the sequence — checked by the oracle
     (x* and f*_k within its duality-gap error)."""
-    from gen.sqp_sequence import apply_dense, sqp_sequence
+    from gen.sqp_sequence import sqp_sequence
+    from oracle.bfgs import rank2_update
     from oracle.ipm import Problem, solve
     q = planted_qp(300, 80, density=0.05, rank=16, seed=3, rows="vmat", var="box")
     ups = sqp_sequence(q, 4, seed=0)
     H = q.H.copy()
     for up in ups:
-        apply_dense(H, up)
+        H = rank2_update(H, up.u, up.alpha, up.v, up.beta)
         r = solve(Problem(H=H, g=up.g.copy(), A=q.A_scipy(), l=q.l, u=q.u, xl=q.xl, xu=q.xu))
         assert r.status == "converged"
         assert np.max(np.abs(r.x - q.x_star)) <= 1e-6

@@ -5,7 +5,8 @@ import pytest
 import torch
 
 from gen.planted import planted_qp
-from gen.sqp_sequence import apply_dense, sqp_sequence
+from gen.sqp_sequence import sqp_sequence
+from oracle.bfgs import rank2_update
 from gen.torch_io import problem_tensors
 from oracle.ipm import Options, Problem, solve, warm_start_point
 
@@ -63,7 +64,7 @@ def test_sqp_sequence_warm_start_matches_oracle(seed):
         assert qp.solve() == "ok"
         sol = qp.solution()
         st = qp.stats()
-        apply_dense(H, up)
+        H = rank2_update(H, up.u, up.alpha, up.v, up.beta)
         p = Problem(H=H, g=up.g.copy(), A=q.A_scipy(), l=q.l, u=q.u, xl=q.xl, xu=q.xu)
         ref = solve(p, Options(), start=warm_start_point(p, ref.x, ref.it.lam, Options()))
         assert ref.status == "converged"

@@ -278,3 +278,137 @@ def test_warm_start_reaches_planted_optimum():
     assert np.max(np.abs(warm.x - cold.x)) <= 1e-6
     best = np.max(np.abs(warm.x - cold.x))
     assert best <= 1e-6
+
+
+# ---------------------------------------------------------------- R15 / R18 / a11 hand pins
+def test_warm_start_point_hand_values():
+    """R15 (SURVEY §8(c) point 15; the paper only names warm starting), values worked by
+    hand for theta = 1e-3 on a 3-variable, 1-row problem:
+      x_prev = (0, 5, 3.5), boxes [0,1], [0,0.002], (-inf,3]:
+        margins min(theta, (xu-xl)/4) = 1e-3, 5e-4, theta (one-sided)  ->  x0 = (1e-3, 1.5e-3, 2.999)
+      s = max(gap(x0), theta): s_lA = max(1e-3+1.5e-3-0.5, theta) = 1e-3; s_lx = (1e-3, 1.5e-3);
+        s_ux = (0.999, max(5e-4, theta) = 1e-3, max(1e-3, theta) = 1e-3)
+      lam = max(lam_prev, theta): lA 0.25; lx (2, 1e-3); ux (1e-3, 0.5, 1e-3)
+      mu0 = 0.1 * sum(lam s) / 6 = 0.1 * 0.0037515 / 6 = 6.2525e-5."""
+    p = Problem(H=np.eye(3), g=np.zeros(3), A=np.array([[1.0, 1.0, 0.0]]), l=np.array([0.5]),
+                u=np.array([np.inf]), xl=np.array([0.0, 0.0, -np.inf]), xu=np.array([1.0, 0.002, 3.0]))
+    lam = {"lA": np.array([0.25]), "uA": np.zeros(0), "lx": np.array([2.0, 0.0]), "ux": np.array([0.0, 0.5, 0.0])}
+    w = warm_start_point(p, np.array([0.0, 5.0, 3.5]), lam, Options())
+    np.testing.assert_allclose(w.x, [1e-3, 1.5e-3, 2.999], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(w.s["lA"], [1e-3], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(w.s["lx"], [1e-3, 1.5e-3], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(w.s["ux"], [0.999, 1e-3, 1e-3], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(w.lam["lA"], [0.25])
+    np.testing.assert_array_equal(w.lam["lx"], [2.0, 1e-3])
+    np.testing.assert_array_equal(w.lam["ux"], [1e-3, 0.5, 1e-3])
+    assert abs(w.mu - 6.2525e-5) <= 1e-18
+
+
+def test_mehrotra_hand_values():
+    """R18 worked by hand on min 1/2 x^2 - x/2, x >= 0 at x = s = lam = 1:
+      affine (r_c = lam s = 1): r_H = x + g - lam = -0.5, Q = 1 + lam/s = 2, r1 = 0.5 - 1 = -0.5,
+        dx = -0.25, ds = -0.25, dlam = -(1 - 0.25) = -0.75; alpha (tau = 1) = 1 for both;
+        mu = 1, mu_aff = (1 - 0.75)(1 - 0.25) = 0.1875, sigma = 0.1875^3 = 27/4096
+      corrector r_c = lam s + dlam_aff ds_aff - sigma mu = 1 + 0.1875 - 27/4096 = 1.180908203125
+        r1 = 0.5 - 1.180908203125, dx = r1 / 2 = -0.3404541015625, dlam = -(r_c + dx) = -0.8404541015625.
+    Squaring sigma instead of cubing it, or dropping the dlam_aff o ds_aff term, changes dx."""
+    from oracle.ipm import _mehrotra
+    e = np.zeros(0)
+    p = Problem(H=np.array([[1.0]]), g=np.array([-0.5]), A=np.zeros((0, 1)), l=e, u=e, xl=np.array([0.0]),
+                xu=np.array([np.inf]))
+    it = Iterate(np.array([1.0]), {"lA": e, "uA": e, "lx": np.array([1.0]), "ux": e},
+                 {"lA": e, "uA": e, "lx": np.array([1.0]), "ux": e}, 0.5)
+    dx, ds, dl, smu = _mehrotra(p, it, Options(predictor_corrector=True))
+    assert smu == 27.0 / 4096.0
+    assert abs(dx[0] - (-0.3404541015625)) <= 1e-15
+    assert abs(ds["lx"][0] - (-0.3404541015625)) <= 1e-15
+    assert abs(dl["lx"][0] - (-0.8404541015625)) <= 1e-15
+
+
+def test_rank2_update_spec_hand_case_and_secant():
+    """a11 / oracle.bfgs: SPEC S:380 hand case (H = I, s = e1, y = 2 e1 -> diag(2, 1, 1)), the
+    secant equation H+ s = y and preserved positive definiteness on a random SPD H."""
+    from oracle.bfgs import bfgs_terms, rank2_update
+    H = np.eye(3)
+    s = np.array([1.0, 0.0, 0.0])
+    Hp = rank2_update(H, *bfgs_terms(H, s, 2.0 * s))
+    np.testing.assert_array_equal(Hp, np.diag([2.0, 1.0, 1.0]))
+    rng = np.random.default_rng(11)
+    M = rng.normal(size=(30, 30))
+    H = M @ M.T + 30 * np.eye(30)
+    s = rng.normal(size=30)
+    y = H @ s + 0.3 * rng.normal(size=30)
+    assert y @ s > 0
+    Hp = rank2_update(H, *bfgs_terms(H, s, y))
+    np.testing.assert_allclose(Hp @ s, y, rtol=0, atol=1e-11 * np.abs(y).max())
+    assert np.linalg.eigvalsh(Hp).min() > 0
+    # y = H s (already consistent): H+ acts identically to H on s (S:378)
+    Hq = rank2_update(H, *bfgs_terms(H, s, H @ s))
+    np.testing.assert_allclose(Hq @ s, H @ s, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- oracle.pcg (textbook Jacobi PCG)
+def _spd(n, seed, cond=50.0):
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.normal(size=(n, n)))
+    return (Q * np.geomspace(1.0, cond, n)) @ Q.T
+
+
+def test_pcg_dense_spd_matches_cholesky():
+    """dense SPD 30x30 against a Cholesky solve (scipy cho_solve)."""
+    import scipy.linalg as sla
+    from oracle.pcg import pcg
+    K = _spd(30, 1)
+    b = np.random.default_rng(2).normal(size=30)
+    res = pcg(lambda v: K @ v, 1.0 / np.diag(K), b, rtol=1e-13)
+    x_ref = sla.cho_solve(sla.cho_factor(K), b)
+    assert not res.breakdown and res.iters <= 3 * 30   # finite precision: a few more than n
+    np.testing.assert_allclose(res.x, x_ref, rtol=0, atol=1e-10 * np.abs(x_ref).max())
+
+
+def test_pcg_identity_and_exact_jacobi_one_iteration():
+    """K = I and K diagonal with the exact Jacobi preconditioner converge in 1 iteration."""
+    from oracle.pcg import pcg
+    b = np.random.default_rng(3).normal(size=17)
+    res = pcg(lambda v: v, np.ones(17), b, rtol=1e-14)
+    assert res.iters == 1 and np.array_equal(res.x, b)
+    d = np.random.default_rng(4).uniform(0.5, 4.0, 17)
+    res = pcg(lambda v: d * v, 1.0 / d, b, rtol=1e-14)
+    assert res.iters == 1
+    np.testing.assert_allclose(res.x, b / d, rtol=1e-15)
+
+
+def test_pcg_conjugacy_and_finite_termination():
+    """CG theory: successive directions are K-conjugate (p_i^T K p_j = 0, i != j), and in exact
+    arithmetic CG terminates in <= n steps (here n = 8: residual at rounding level after 8)."""
+    from oracle.pcg import pcg
+    K = _spd(8, 5, cond=20.0)
+    b = np.random.default_rng(6).normal(size=8)
+    Minv = 1.0 / np.diag(K)
+    res = pcg(lambda v: K @ v, Minv, b, maxit=8, keep_directions=True)
+    P = np.array(res.directions)
+    G = P @ K @ P.T
+    off = G - np.diag(np.diag(G))
+    assert np.abs(off).max() <= 1e-10 * np.abs(np.diag(G)).max()
+    assert np.linalg.norm(res.r) <= 1e-10 * np.linalg.norm(b)
+    # one hand-checkable iteration: x1 = alpha0 z0 with alpha0 = (r0,z0)/(K z0, z0)
+    r1 = pcg(lambda v: K @ v, Minv, b, maxit=1)
+    z0 = Minv * b
+    assert abs(r1.alpha - (b @ z0) / (z0 @ K @ z0)) <= 1e-15 * abs(r1.alpha)
+    np.testing.assert_allclose(r1.x, r1.alpha * z0, rtol=1e-15)
+
+
+def test_pcg_on_condensed_operator_matches_condensed_cholesky():
+    """The oracle PCG on K = H + Sigma_b + A^T Sigma_c A (oracle.kkt.condensed_apply) reaches the
+    Cholesky solution of oracle.kkt.condensed_matrix."""
+    from oracle.pcg import pcg
+    q = config("C1", 3)
+    rng = np.random.default_rng(7)
+    A = q.A_scipy().toarray()
+    sb = rng.uniform(0.0, 3.0, q.n)
+    sc = 10.0 ** rng.uniform(-2, 2, q.m)
+    b = rng.normal(size=q.n)
+    K = okkt.condensed_matrix(q.H, A, sb, sc)
+    res = pcg(lambda v: okkt.condensed_apply(q.H, A, sb, sc, v), 1.0 / okkt.jacobi_diag(q.H, A, sb, sc), b,
+              rtol=1e-13)
+    np.testing.assert_allclose(res.x, np.linalg.solve(K, b), rtol=0, atol=1e-9 * np.abs(res.x).max())
