@@ -15,7 +15,8 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["linalg.cu", "compact.cu", "pcg.cu", "ipmops.cu", "shard.cu", "comm.cu", "ipm_api.cu", "sqp.cu"]
+SOURCES = ["linalg.cu", "compact.cu", "pcg.cu", "ipmops.cu", "shard.cu", "peer.cu", "comm.cu", "ipm_api.cu",
+           "sqp.cu"]
 
 
 def _stale(out: str, deps) -> bool:

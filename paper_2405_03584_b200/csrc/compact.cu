@@ -155,4 +155,18 @@ void launch_compact_append(const Prob &P, double *U, int col, const double *u, c
                                                                                                      col, u, v);
 }
 
+
+// Touch every kernel once (cudaFuncGetAttributes) so that CUDA's lazy module loading never
+// has to load one while a peer-exchange wait kernel spins on the device (kernels.h).
+template <class F>
+static void touch_kernel(F f) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(f));
+}
+
+void preload_compact() {
+    touch_kernel(k_compact_ut); touch_kernel(k_compact_us); touch_kernel(k_compact_diag);
+    touch_kernel(k_compact_append);
+}
+
 }  // namespace ipm

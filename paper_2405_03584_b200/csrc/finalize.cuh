@@ -81,4 +81,71 @@ __device__ __forceinline__ void fin_resid(Scalars *sc, double rh, double prim, d
     if (!finite_d(obj)) sc->nonfinite = 1;
 }
 
+// Rank-ordered combination of every rank's partials of one XStage (row-sharded mode; one
+// thread): the same epilogue the single-GPU last blocks apply, so every rank takes
+// bit-identical decisions.  xa[r * 8 + k] = rank r's Scalars::loc[k].  Used by k_xcombine
+// (allgather data plane) and by the peer-memory wait kernel (peer.cu).
+__device__ __forceinline__ void xcombine_apply(Scalars *sc, const double *xa, int P, int stage, double p0, double p1,
+                                               int64_t p2) {
+    auto sum = [&](int k) {
+        double s = 0.0;
+        for (int r = 0; r < P; ++r) s += xa[r * 8 + k];
+        return s;
+    };
+    auto mx = [&](int k) {
+        double s = xa[k];
+        for (int r = 1; r < P; ++r) s = fmax(s, xa[r * 8 + k]);
+        return s;
+    };
+    auto mn = [&](int k) {
+        double s = xa[k];
+        for (int r = 1; r < P; ++r) s = fmin(s, xa[r * 8 + k]);
+        return s;
+    };
+    switch (stage) {
+        case X_PCG_INIT:
+            fin_pcg_init(sc, sum(2), sum(3), p0, p1, p2);
+            break;
+        case X_PCG_ALPHA: {
+            if (sc->done) return;
+            double s = 0.0, sb = 0.0, sh = 0.0;
+            for (int r = 0; r < P; ++r) {
+                s += xa[r * 8 + 0] + xa[r * 8 + 1];
+                sb += xa[r * 8 + 0];
+                sh += xa[r * 8 + 1];
+            }
+            sc->S_b = sb;
+            sc->S_H = sh;
+            fin_pcg_alpha(sc, s + sc->S_c);
+            break;
+        }
+        case X_PCG_UPDATE:
+            if (sc->done) return;
+            fin_pcg_update(sc, sum(2), sum(3));
+            break;
+        case X_PCG_RESTART:
+            fin_pcg_restart(sc, sum(2), sum(3));
+            break;
+        case X_RES2:
+            sc->res2 = sum(4);
+            break;
+        case X_SUMLS:
+            sc->sum_ls = sc->sum_ls_m + sum(5);
+            break;
+        case X_RESID:
+            if (mx(6) > 0.0) sc->nonfinite = 1;
+            fin_resid(sc, mx(0), mx(1), mx(2), mx(3), sum(4));
+            break;
+        case X_RECOVER:
+            fin_recover(sc, mn(0), mn(1), p0);
+            break;
+        case X_MUAFF:
+            sc->muaff = sc->muaff_m + sum(5);
+            break;
+        default:
+            break;
+    }
+}
+
+
 }  // namespace ipm

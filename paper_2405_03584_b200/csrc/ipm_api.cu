@@ -5,6 +5,7 @@
 // every iteration, P:232-238 — here only ~20 scalars come back per IPM iteration for the
 // mu logic of Alg. 1 lines 10-15).  The PCG inner loop (line 2) is a CUDA graph whose
 // conditional WHILE node is re-armed by the device, so a whole PCG solve is one launch.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,8 +17,11 @@
 #include <vector>
 
 #include "../../include/ipm.h"
+#include <unistd.h>
+
 #include "comm.h"
 #include "kernels.h"
+#include "peer.h"
 #include "state.h"
 
 #define IPM_EXPORT extern "C" __attribute__((visibility("default")))
@@ -74,7 +78,7 @@ struct Offsets {
     size_t nvec[40];
     size_t mvec[40];
     size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad, gfull, xloc_all;
-    size_t ch0, cw, cs, cspart, chpart, symr, symt, symz, zcol, zvec, zall, hashes;
+    size_t ch0, cw, cs, cspart, chpart, symr, symt, symz, zcol, zvec, zall, hashes, peer;
     int n_nvec, n_mvec;
     int nchunk;
 };
@@ -124,6 +128,8 @@ Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks
     o.bad = L.take(sizeof(unsigned long long));
     o.gfull = L.take(sizeof(double) * ((size_t)chunk * nranks + 2));
     o.xloc_all = L.take(sizeof(double) * 8 * (size_t)nranks);
+    // peer-memory data plane (peer.h): the region other ranks store into (sharded only)
+    o.peer = L.take(nranks > 1 && nranks <= kPeerMax ? peer_layout(ncols, nranks).bytes : 256);
     return o;
 }
 
@@ -172,6 +178,10 @@ struct ipm_ctx {
     ipm::Comm *comm = nullptr;
     bool sharded = false;
     int64_t chunk = 0;
+    // peer-memory data plane (peer.h): device-side exchanges instead of Comm allgathers
+    bool peer_on = false;
+    ipm::PeerArgs peer{};
+    std::vector<void *> ipc_opened;
 };
 
 namespace {
@@ -207,10 +217,101 @@ ipm_status fail(ipm_ctx *c, ipm_status s, const char *fmt, ...) {
         if (s_ != IPM_OK) return s_;       \
     } while (0)
 
+// Peer-memory data plane setup (peer.h): exchange the peer regions' addresses over the Comm
+// (bootstrap only) — raw pointers between ranks of one process (peer access enabled across
+// devices), CUDA IPC handles between processes — and point V.gfull at the region's gfull.
+// IPM_PEER=0 (experiment switch) keeps the Comm allgather data plane.
+using DrvGetAddressRange = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+ipm_status setup_peer(ipm_ctx *ctx, char *region, char *scratch) {
+    const int R = ctx->comm->nranks, me = ctx->comm->rank;
+    const char *env = getenv("IPM_PEER");
+    if (R < 2 || R > kPeerMax || (env && atoi(env) == 0)) return IPM_OK;
+    struct Ex {
+        cudaIpcMemHandle_t h;
+        int64_t off;
+        uint64_t raw;
+        int32_t pid, dev;
+    };
+    Ex mine{};
+    mine.raw = reinterpret_cast<uint64_t>(region);
+    mine.pid = (int32_t)getpid();
+    mine.dev = ctx->device;
+    {   // CUDA IPC needs the allocation base (the workspace may be a sub-allocation of torch's pool)
+        static DrvGetAddressRange range = nullptr;
+        if (!range) {
+            cudaDriverEntryPointQueryResult q;
+            void *fn = nullptr;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                range = reinterpret_cast<DrvGetAddressRange>(fn);
+        }
+        CUdeviceptr base = 0;
+        size_t sz = 0;
+        if (!range || range(&base, &sz, reinterpret_cast<CUdeviceptr>(region)) != CUDA_SUCCESS)
+            return fail(ctx, IPM_ERR_CUDA, "cuMemGetAddressRange failed on the workspace");
+        mine.off = (int64_t)(reinterpret_cast<CUdeviceptr>(region) - base);
+        if (cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void *>(base)) != cudaSuccess) {
+            cudaGetLastError();
+            std::memset(&mine.h, 0, sizeof mine.h);   // same-process groups do not need it
+        }
+    }
+    Ex *dsend = reinterpret_cast<Ex *>(scratch);
+    Ex *drecv = dsend + 1;
+    CK(cudaMemcpyAsync(dsend, &mine, sizeof mine, cudaMemcpyHostToDevice, ctx->st));
+    std::string e;
+    if (ctx->comm->allgather(dsend, drecv, sizeof(Ex), ctx->st, e)) return fail(ctx, IPM_ERR_NCCL, "%s", e.c_str());
+    std::vector<Ex> all(R);
+    CK(cudaMemcpyAsync(all.data(), drecv, sizeof(Ex) * R, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    PeerArgs pa{};
+    if (const char *t = getenv("IPM_PEER_TIMEOUT_S")) pa.timeout_ns = (unsigned long long)(atof(t) * 1e9);
+    pa.rank = me;
+    pa.P = R;
+    pa.chunk = ctx->chunk;
+    pa.L = peer_layout(ctx->n, R);
+    for (int r = 0; r < R; ++r) {
+        if (r == me) {
+            pa.base[r] = region;
+        } else if (all[r].pid == mine.pid) {
+            if (all[r].dev != ctx->device) {
+                const cudaError_t pe = cudaDeviceEnablePeerAccess(all[r].dev, 0);
+                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(ctx, IPM_ERR_CUDA, "peer access %d -> %d: %s", ctx->device, all[r].dev,
+                                cudaGetErrorString(pe));
+                cudaGetLastError();
+            }
+            pa.base[r] = reinterpret_cast<char *>(all[r].raw);
+        } else {
+            void *ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, all[r].h, cudaIpcMemLazyEnablePeerAccess));
+            ctx->ipc_opened.push_back(ptr);
+            pa.base[r] = static_cast<char *>(ptr) + all[r].off;
+        }
+    }
+    ctx->peer = pa;
+    ctx->peer_on = true;
+    ctx->V.gfull = reinterpret_cast<double *>(region + pa.L.gfull);
+    // everybody's region is zeroed (workspace memset) before anyone may store into it
+    CK(cudaStreamSynchronize(ctx->st));
+    if (ctx->comm->allgather(dsend, drecv, sizeof(Ex), ctx->st, e)) return fail(ctx, IPM_ERR_NCCL, "%s", e.c_str());
+    CK(cudaStreamSynchronize(ctx->st));
+    return IPM_OK;
+}
+
+ipm_status peer_timeout_error(ipm_ctx *ctx) {
+    const unsigned long long *d = ctx->hsc->peer_diag;
+    return fail(ctx, IPM_ERR_NCCL,
+                "peer exchange timed out on rank %d: exchange %llu (stage %lld) never arrived from rank %llu "
+                "(its flag = %llu)",
+                ctx->peer.rank, d[0], (long long)d[3] - 1000, d[1], d[2]);
+}
+
 ipm_status sync_scalars(ipm_ctx *ctx) {
     CKL();
     CK(cudaMemcpyAsync(ctx->hsc, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    if (ctx->peer_on && ctx->hsc->peer_timeout) return peer_timeout_error(ctx);
     return IPM_OK;
 }
 
@@ -247,9 +348,19 @@ void assign_vectors(ipm_ctx *c, const Offsets &o) {
 // ------------------------------------------------------------------- sharded collectives
 // Full-length copy of an x-space vector: the vector itself on one GPU, else an allgather of
 // every rank's chunk into V.gfull (rank r's rows land at [r*chunk, ...), i.e. global order).
-ipm_status gather(ipm_ctx *ctx, const double *local, const double **full) {
+ipm_status gather(ipm_ctx *ctx, const double *local, const double **full, cudaStream_t st = nullptr,
+                  int check_done = 0) {
     if (!ctx->sharded) {
         *full = local;
+        return IPM_OK;
+    }
+    if (ctx->peer_on) {                // every rank stores its slice into every peer's gfull (peer.h)
+        st = st ? st : ctx->st;
+        launch_peer_put_vec(ctx->peer, local, ctx->nloc, ctx->sc, check_done, st);
+        launch_peer_wait(ctx->peer, ctx->sc, -1, 0.0, 0.0, 0, check_done, 0, 0, st);
+        ctx->launches += 2;
+        CKL();
+        *full = ctx->V.gfull;          // = the peer region's gfull
         return IPM_OK;
     }
     std::string e;
@@ -262,9 +373,18 @@ ipm_status gather(ipm_ctx *ctx, const double *local, const double **full) {
 // Sharded symmetric GEMV: the column parts this rank computed for other ranks' rows (zpart)
 // are reduced to a full-length vector, allgathered, and each rank adds the P contributions to
 // its rows in rank order into the last ypart slot (shard.cu).  No-op otherwise.
-ipm_status sym_exchange(ipm_ctx *ctx) {
+ipm_status sym_exchange(ipm_ctx *ctx, cudaStream_t st = nullptr, int check_done = 0) {
     if (!ctx->sym_sharded) return IPM_OK;
     const Prob &P = ctx->P;
+    if (ctx->peer_on) {                // fused zreduce + scatter to the owning ranks, wait, fold
+        st = st ? st : ctx->st;
+        launch_peer_zput(ctx->peer, ctx->sym_zrows, P.sym_ldz, P.sym_z, ctx->sym_zcol, ctx->sc, check_done, st);
+        launch_peer_wait(ctx->peer, ctx->sc, -1, 0.0, 0.0, 0, check_done, 0, 0, st);
+        launch_peer_zfold(ctx->peer, P.n, ctx->V.ypart, ctx->ncb, ctx->sc, check_done, st);
+        ctx->launches += 3;
+        CKL();
+        return IPM_OK;
+    }
     launch_zreduce(ctx->sym_zrows, P.sym_ldz, P.sym_z, ctx->sym_zcol, ctx->sym_zvec, ctx->st);
     CKL();
     std::string e;
@@ -277,8 +397,17 @@ ipm_status sym_exchange(ipm_ctx *ctx) {
 }
 
 // Combine this stage's per-rank partials (Scalars::loc) across ranks (shard.cu).
-ipm_status xcombine(ipm_ctx *ctx, int stage, double p0 = 0.0, double p1 = 0.0, int64_t p2 = 0) {
+ipm_status xcombine(ipm_ctx *ctx, int stage, double p0 = 0.0, double p1 = 0.0, int64_t p2 = 0,
+                    cudaStream_t st = nullptr, int check_done = 0, cudaGraphConditionalHandle h = 0, int use_cond = 0) {
     if (!ctx->sharded) return IPM_OK;
+    if (ctx->peer_on) {                // this rank's partials into every peer's xall[stage]; wait + combine
+        st = st ? st : ctx->st;
+        launch_peer_put_loc(ctx->peer, stage, ctx->sc, check_done, st);
+        launch_peer_wait(ctx->peer, ctx->sc, stage, p0, p1, p2, check_done, h, use_cond, st);
+        ctx->launches += 2;
+        CKL();
+        return IPM_OK;
+    }
     std::string e;
     if (ctx->comm->allgather(ctx->sc->loc, ctx->V.xloc_all, sizeof(double) * 8, ctx->st, e))
         return fail(ctx, IPM_ERR_NCCL, "%s", e.c_str());
@@ -328,18 +457,21 @@ ipm_status op_apply(ipm_ctx *ctx, const double *v_local, const double *v_full, d
 }
 
 // One PCG iteration on a row-sharded context (no graph: collectives between the kernels).
-ipm_status pcg_iteration_sharded(ipm_ctx *ctx) {
+// st = nullptr: the context stream (host-driven); otherwise the graph-capture stream, and with
+// use_cond the last exchange sets the WHILE condition (peer data plane only: no host calls).
+ipm_status pcg_iteration_sharded(ipm_ctx *ctx, cudaStream_t st = nullptr, int use_cond = 0) {
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
-    launch_pcg_p(P, V, ctx->sc, ctx->st);
+    st = st ? st : ctx->st;
+    launch_pcg_p(P, V, ctx->sc, st);
     const double *pf = nullptr;
-    TRY(gather(ctx, V.pp, &pf));
-    launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, ctx->st, kMaxGrid, side_block());
-    launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, ctx->st);
-    TRY(sym_exchange(ctx));
-    TRY(xcombine(ctx, X_PCG_ALPHA));
-    launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, ctx->st);
-    TRY(xcombine(ctx, X_PCG_UPDATE));
+    TRY(gather(ctx, V.pp, &pf, st, 1));
+    launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, st, kMaxGrid, side_block());
+    launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, st);
+    TRY(sym_exchange(ctx, st, 1));
+    TRY(xcombine(ctx, X_PCG_ALPHA, 0.0, 0.0, 0, st, 1));
+    launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, st);
+    TRY(xcombine(ctx, X_PCG_UPDATE, 0.0, 0.0, 0, st, 1, ctx->handle, use_cond));
     ctx->launches += 3 + (P.m > 0 ? 2 : 0);
     CKL();
     return IPM_OK;
@@ -362,9 +494,14 @@ ipm_status build_graph(ipm_ctx *ctx) {
     // early-exits in every kernel (sc->done), and the last update sets the condition
     const char *ue = getenv("IPM_UNROLL");
     const int unroll = ue ? std::max(1, std::min(8, atoi(ue))) : 1;
-    for (int u = 0; u < unroll; ++u)
-        launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle, 1,
-                             ctx->cap, &ctx->fork, ctx->fused_p);
+    if (ctx->sharded) {
+        // peer data plane: the whole sharded iteration (puts, waits, combines) is device-side
+        TRY(pcg_iteration_sharded(ctx, ctx->cap, 1));
+    } else {
+        for (int u = 0; u < unroll; ++u)
+            launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle,
+                                 1, ctx->cap, &ctx->fork, ctx->fused_p);
+    }
     cudaGraph_t captured = nullptr;
     CK(cudaStreamEndCapture(ctx->cap, &captured));
     CK(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
@@ -408,11 +545,13 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) 
     }
     ctx->have_dx = true;
     const bool small = !ctx->sharded && !P.aug && !P.hess_compact && P.n <= kSmallN && ctx->opt.use_graph;
-    const bool graph = ctx->opt.use_graph && !ctx->sharded && !small;
+    const bool graph = ctx->opt.use_graph && (!ctx->sharded || ctx->peer_on) && !small;
     if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
     int64_t it_prev = 0;
-    const int per_it = (ctx->fused_p ? 2 : 3) + (P.m > 0 ? 2 : 0);   // kernels per PCG iteration
+    // kernels per PCG iteration (sharded peer plane: + 2 per exchange, + zfold)
+    const int per_it = (ctx->fused_p ? 2 : 3) + (P.m > 0 ? 2 : 0) +
+                       (ctx->sharded && ctx->peer_on ? 6 + (ctx->sym_sharded ? 3 : 0) : 0);
     for (int round = 0;; ++round) {
         if (ctx->fused_p && !small) {
             launch_pcg_p(P, V, ctx->sc, ctx->st);           // p = z after the (re)start; S_b
@@ -426,6 +565,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) 
         } else if (graph) {
             CK(cudaGraphLaunch(ctx->gexec, ctx->st));
             TRY(sync_scalars(ctx));
+            if (ctx->hsc->peer_timeout) return peer_timeout_error(ctx);
         } else if (ctx->sharded) {
             // host-driven batches; every rank sees the same combined `done`, so all ranks run
             // the same number of iterations and collectives
@@ -796,6 +936,10 @@ IPM_EXPORT void ipm_group_destroy(ipm_group *g) {
 }
 
 static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspace, ipm_stream_t stream) {
+    // load every kernel now: CUDA's lazy loading must never run while a peer-exchange wait
+    // kernel of another rank sharing this device spins (it would wait for that kernel)
+    preload_all_kernels();
+    cudaGetLastError();
     ctx->st = reinterpret_cast<cudaStream_t>(stream);
     ctx->n = p->n;
     ctx->m = p->m;
@@ -865,6 +1009,7 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             ctx->chunk = (p->n + ctx->comm->nranks - 1) / ctx->comm->nranks;
             const int64_t one = 1;
             CK(cudaMemcpyAsync(&ctx->sc->sharded, &one, sizeof one, cudaMemcpyHostToDevice, ctx->st));
+            if ((s = setup_peer(ctx, ctx->ws + o.peer, ctx->ws + o.part)) != IPM_OK) return s;
         }
         Prob &P = ctx->P;
         P.n = (int)nloc;
@@ -1403,6 +1548,7 @@ IPM_EXPORT void ipm_destroy(ipm_ctx *ctx) {
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->hsc) cudaFreeHost(ctx->hsc);
+    for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     delete ctx->comm;
     delete ctx;
 }

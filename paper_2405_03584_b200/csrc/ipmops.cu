@@ -663,4 +663,22 @@ void launch_muaff(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
                                                      V.lam_ux, V.adl_ux, V.part[1], sc, C_MUAFF_N, 1);
 }
 
+
+// Touch every kernel once (cudaFuncGetAttributes) so that CUDA's lazy module loading never
+// has to load one while a peer-exchange wait kernel spins on the device (kernels.h).
+template <class F>
+static void touch_kernel(F f) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(f));
+}
+
+void preload_ipmops() {
+    touch_kernel(k_init_x); touch_kernel(k_init_slacks); touch_kernel(k_sum_ls); touch_kernel(k_resid_m);
+    touch_kernel(k_sigma_m); touch_kernel(k_rhs_m); touch_kernel(k_recover_m); touch_kernel(k_recover_n);
+    touch_kernel(k_update); touch_kernel(k_muaff);
+#define IPM_TOUCH_G(GG) touch_kernel(k_resid_n<GG>); touch_kernel(k_sigma_n_jacobi<GG>); touch_kernel(k_rhs_n<GG>);
+    IPM_TOUCH_G(4) IPM_TOUCH_G(8) IPM_TOUCH_G(16) IPM_TOUCH_G(32)
+#undef IPM_TOUCH_G
+}
+
 }  // namespace ipm

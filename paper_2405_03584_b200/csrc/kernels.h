@@ -86,6 +86,21 @@ int spmv_keep();    // 1: PCG-mode SpMV / SpMV^T load A, A^T with an L2 evict_la
 void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
 cudaError_t configure_linalg_attrs();   // >48 KB dynamic smem opt-ins (per device: called at every create)
 cudaError_t configure_pcg_attrs();
+// force-load every kernel (CUDA lazy loading must not run while a peer wait kernel spins)
+void preload_linalg();
+void preload_pcg();
+void preload_ipmops();
+void preload_shard();
+void preload_peer();
+void preload_compact();
+inline void preload_all_kernels() {
+    preload_linalg();
+    preload_pcg();
+    preload_ipmops();
+    preload_shard();
+    preload_peer();
+    preload_compact();
+}
 void configure_pcg_carveout();
 // NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,
 // yu = -A px + D_u pu (masked); mode 1 (PCG): done check + S_c = a.t + pl.yl + pu.yu

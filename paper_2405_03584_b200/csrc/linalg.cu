@@ -1267,4 +1267,28 @@ void configure_linalg_carveout() {
     cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
 }
 
+
+// Touch every kernel once (cudaFuncGetAttributes) so that CUDA's lazy module loading never
+// has to load one while a peer-exchange wait kernel spins on the device (kernels.h).
+template <class F>
+static void touch_kernel(F f) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(f));
+}
+
+void preload_linalg() {
+    touch_kernel(k_gemv_tiles<true, 0>); touch_kernel(k_gemv_tiles<true, 1>);
+    touch_kernel(k_gemv_tiles<false, 0>); touch_kernel(k_gemv_tiles<false, 1>);
+    touch_kernel(k_gemv_bulk<0>); touch_kernel(k_gemv_bulk<1>);
+    touch_kernel(k_symv_bulk<0>); touch_kernel(k_symv_bulk<1>);
+    touch_kernel(k_count_asym); touch_kernel(k_spmv<0>); touch_kernel(k_spmv<1>);
+    touch_kernel(k_spmv_aug<0>); touch_kernel(k_spmv_aug<1>);
+#define IPM_TOUCH_G(GG) touch_kernel(k_apply_reduce<GG, 0>); touch_kernel(k_apply_reduce<GG, 1>); \
+    touch_kernel(k_apply_reduce<GG, 2>); touch_kernel(k_jacobi<GG>);
+    IPM_TOUCH_G(4) IPM_TOUCH_G(8) IPM_TOUCH_G(16) IPM_TOUCH_G(32)
+#undef IPM_TOUCH_G
+    touch_kernel(k_diag_extract); touch_kernel(k_count_nonfinite); touch_kernel(k_tr_count);
+    touch_kernel(k_tr_scan); touch_kernel(k_tr_fill); touch_kernel(k_rank2);
+}
+
 }  // namespace ipm

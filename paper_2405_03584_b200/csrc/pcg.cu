@@ -865,4 +865,24 @@ void configure_pcg_carveout() {
     cudaFuncSetAttribute(k_pcg_p, cudaFuncAttributePreferredSharedMemoryCarveout, c);
 }
 
+
+// Touch every kernel once (cudaFuncGetAttributes) so that CUDA's lazy module loading never
+// has to load one while a peer-exchange wait kernel spins on the device (kernels.h).
+template <class F>
+static void touch_kernel(F f) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(f));
+}
+
+void preload_pcg() {
+    touch_kernel(k_pcg_init); touch_kernel(k_pcg_restart); touch_kernel(k_dot2); touch_kernel(k_pcg_p);
+    touch_kernel(k_pcg_update<4>); touch_kernel(k_pcg_update<8>); touch_kernel(k_pcg_update<16>);
+    touch_kernel(k_pcg_update<32>);
+    touch_kernel(k_pcg_update_fp<4, false, kBlock>); touch_kernel(k_pcg_update_fp<8, false, kBlock>);
+    touch_kernel(k_pcg_update_fp<4, true, kBlock>); touch_kernel(k_pcg_update_fp<8, true, kBlock>);
+    touch_kernel(k_pcg_update_fp<4, true, 1024>); touch_kernel(k_pcg_update_fp<8, true, 1024>);
+    touch_kernel(k_pcg_small);
+    touch_kernel(k_spmvT<4>); touch_kernel(k_spmvT<8>); touch_kernel(k_spmvT<16>); touch_kernel(k_spmvT<32>);
+}
+
 }  // namespace ipm

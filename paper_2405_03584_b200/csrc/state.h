@@ -46,6 +46,11 @@ struct Scalars {
     // produces the global values.  Slot use per stage is documented in shard.cu.
     int64_t sharded;
     double loc[8];
+    // peer-memory data plane (peer.cu): sequence number of the last completed exchange, the
+    // put kernels' arrival counter, and a timeout flag (a peer never arrived)
+    unsigned long long peer_seq;
+    unsigned int peer_ctr, peer_timeout;
+    unsigned long long peer_diag[4];     // timeout: {expected seq, sender, its flag, stage + 1000}
     unsigned int counters[kNumCounters];
     // --- live launch timing of the PCG operator kernel (bench.py roofline) ---------------
     // kt_neg = max over CTAs of ~(start %globaltimer) (so 0 = unset), reset by the last CTA,
