@@ -114,8 +114,16 @@ typedef struct {
      * (each rank copies its slice).  comm_kind: 0 = none (nranks must be 1); 1 = NCCL,
      * comm_handle_host -> ncclUniqueId (128 bytes, from ipm_nccl_unique_id on rank 0,
      * broadcast by the caller); 2 = in-process group, comm_handle_host = ipm_group* (one host
-     * thread per rank must drive its context).  comm_kind 2 with nranks 1 runs the sharded
-     * code path on one context (testing).  ipm_create is COLLECTIVE when sharded: all ranks
+     * thread per rank must drive its context); 3 = caller-provided host allgather,
+     * comm_handle_host = ipm_host_comm* (any transport: e.g. a gloo process group).
+     * comm_kind 2 with nranks 1 runs the sharded code path on one context (testing).
+     * DATA PLANE: with 2 <= nranks <= 8 every per-iteration exchange runs over peer memory
+     * (each rank stores into the others' workspace regions over NVLink / NVSwitch; the regions'
+     * addresses are exchanged once at create over the comm — CUDA IPC between processes, so the
+     * workspace must be cudaMalloc memory, not a VMM/expandable-segment allocation); the comm
+     * itself (NCCL, group or host callback) is then used only at create.  comm_kind 3 requires
+     * this peer plane.  The environment switch IPM_PEER=0 keeps the comm allgathers instead
+     * (comm_kind 1 / 2 only).  ipm_create is COLLECTIVE when sharded: all ranks
      * must call it concurrently (communicator setup and the exchange of the H-symmetry
      * certificate that selects the sharded symmetric GEMV for an exactly symmetric H with an
      * even chunk; every rank takes the same decision). */
@@ -138,6 +146,16 @@ typedef struct {
 } ipm_problem;
 
 typedef struct ipm_group ipm_group;  /* in-process rank group (comm_kind 2) */
+
+/* comm_kind 3: the caller's host allgather.  allgather(send, recv, bytes, user) must gather
+ * `bytes` from every rank into recv (rank r's block at offset r * bytes) and return 0; it is
+ * called only inside ipm_create (collective), never during a solve. */
+typedef int32_t (*ipm_host_allgather_fn)(const void *send_host, void *recv_host, size_t bytes, void *user);
+typedef struct {
+    int32_t rank, nranks;
+    ipm_host_allgather_fn allgather;
+    void *user;
+} ipm_host_comm;
 
 typedef struct {
     int32_t status;             /* final ipm_status of the last ipm_solve */

@@ -44,6 +44,14 @@ class ipm_problem(C.Structure):
                 ("U", C.c_void_p), ("w", C.c_void_p)]
 
 
+# comm_kind 3 (include/ipm.h ipm_host_comm): the caller's host allgather, used only at create
+IPM_HOST_ALLGATHER = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class ipm_host_comm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("allgather", IPM_HOST_ALLGATHER), ("user", C.c_void_p)]
+
+
 class ipm_stats(C.Structure):
     _fields_ = [("status", C.c_int32), ("ipm_iters", C.c_int32), ("pcg_iters_total", C.c_int64),
                 ("pcg_iters_max", C.c_int32), ("pcg_stalls", C.c_int32), ("pcg_restarts", C.c_int32),

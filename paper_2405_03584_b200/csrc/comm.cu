@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cstring>
 
+#include "../../include/ipm.h"
 #include "comm.h"
 
 bool ipm_group::barrier() {
@@ -114,6 +115,46 @@ Comm *make_nccl_comm(const void *unique_id, int rank, int nranks, std::string &e
         delete c;
         return nullptr;
     }
+    return c;
+}
+
+// ------------------------------------------------------------------------------ host callback
+namespace {
+struct HostComm : Comm {
+    ipm_host_comm hc{};
+    int allgather(const void *send, void *recv, size_t bytes, cudaStream_t st, std::string &err) override {
+        std::vector<unsigned char> s(bytes), r(bytes * (size_t)nranks);
+        cudaError_t e = cudaMemcpyAsync(s.data(), send, bytes, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            err = std::string("host allgather staging: ") + cudaGetErrorString(e);
+            return 1;
+        }
+        if (hc.allgather(s.data(), r.data(), bytes, hc.user) != 0) {
+            err = "host allgather callback failed";
+            return 1;
+        }
+        e = cudaMemcpyAsync(recv, r.data(), r.size(), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // r is a stack buffer
+        if (e != cudaSuccess) {
+            err = std::string("host allgather staging: ") + cudaGetErrorString(e);
+            return 1;
+        }
+        return 0;
+    }
+};
+}  // namespace
+
+Comm *make_host_comm(const void *host_comm, std::string &err) {
+    const ipm_host_comm *h = static_cast<const ipm_host_comm *>(host_comm);
+    if (!h || !h->allgather || h->nranks < 1 || h->rank < 0 || h->rank >= h->nranks) {
+        err = "bad ipm_host_comm";
+        return nullptr;
+    }
+    HostComm *c = new HostComm();
+    c->hc = *h;
+    c->rank = h->rank;
+    c->nranks = h->nranks;
     return c;
 }
 

@@ -43,6 +43,9 @@ struct Comm {
 };
 
 Comm *make_nccl_comm(const void *unique_id, int rank, int nranks, std::string &err);
+// comm_kind 3: the caller's host allgather callback (ipm_host_comm, include/ipm.h) — used only
+// to bootstrap the peer-memory data plane and for the create-time certificate exchange
+Comm *make_host_comm(const void *host_comm, std::string &err);
 Comm *make_local_comm(ipm_group *g, int rank, std::string &err);
 int nccl_unique_id(void *out, size_t bytes, std::string &err);
 

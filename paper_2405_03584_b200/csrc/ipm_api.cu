@@ -878,10 +878,11 @@ static int eff_ranks(const ipm_problem *p) { return p->comm_kind != 0 ? std::max
 // Rows of rank r under the equal-chunk partition (header: chunk = ceil(n / nranks)).
 static ipm_status check_partition(const ipm_problem *p) {
     if (p->comm_kind == 0) {
-        if (p->nranks > 1) return fail(nullptr, IPM_ERR_INVALID, "nranks > 1 needs comm_kind 1 (NCCL) or 2 (local group)");
+        if (p->nranks > 1)
+            return fail(nullptr, IPM_ERR_INVALID, "nranks > 1 needs comm_kind 1 (NCCL), 2 (local group) or 3 (host)");
         return IPM_OK;
     }
-    if (p->comm_kind != 1 && p->comm_kind != 2) return fail(nullptr, IPM_ERR_INVALID, "unknown comm_kind");
+    if (p->comm_kind < 1 || p->comm_kind > 3) return fail(nullptr, IPM_ERR_INVALID, "unknown comm_kind");
     if (!p->comm_handle_host) return fail(nullptr, IPM_ERR_INVALID, "comm_handle_host is null");
     const int64_t P = std::max(1, p->nranks);
     if (p->rank < 0 || p->rank >= P) return fail(nullptr, IPM_ERR_INVALID, "rank out of range");
@@ -997,11 +998,13 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         assign_vectors(ctx, o);
         if (p->comm_kind != 0) {
             std::string e;
-            ctx->comm = (p->comm_kind == 1)
-                            ? ipm::make_nccl_comm(p->comm_handle_host, p->rank, std::max(1, p->nranks), e)
-                            : ipm::make_local_comm(const_cast<ipm_group *>(
-                                                       static_cast<const ipm_group *>(p->comm_handle_host)),
-                                                   p->rank, e);
+            ctx->comm = (p->comm_kind == 1)   ? ipm::make_nccl_comm(p->comm_handle_host, p->rank,
+                                                                        std::max(1, p->nranks), e)
+                        : (p->comm_kind == 3) ? ipm::make_host_comm(p->comm_handle_host, e)
+                                              : ipm::make_local_comm(const_cast<ipm_group *>(
+                                                                         static_cast<const ipm_group *>(
+                                                                             p->comm_handle_host)),
+                                                                     p->rank, e);
             if (!ctx->comm) return fail(ctx, IPM_ERR_NCCL, "communicator: %s", e.c_str());
             if (ctx->comm->nranks != std::max(1, p->nranks))
                 return fail(ctx, IPM_ERR_INVALID, "group size %d != nranks %d", ctx->comm->nranks, p->nranks);
@@ -1010,6 +1013,9 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             const int64_t one = 1;
             CK(cudaMemcpyAsync(&ctx->sc->sharded, &one, sizeof one, cudaMemcpyHostToDevice, ctx->st));
             if ((s = setup_peer(ctx, ctx->ws + o.peer, ctx->ws + o.part)) != IPM_OK) return s;
+            if (p->comm_kind == 3 && !ctx->peer_on && ctx->comm->nranks > 1)
+                return fail(ctx, IPM_ERR_INVALID, "comm_kind 3 needs the peer data plane (2 <= nranks <= %d, "
+                            "IPM_PEER not 0)", kPeerMax);
         }
         Prob &P = ctx->P;
         P.n = (int)nloc;

@@ -57,6 +57,38 @@ def nccl_shard(rank: int, nranks: int, uid: bytes) -> dict:
     return dict(rank=rank, nranks=nranks, comm_kind=1, handle=C.cast(buf, C.c_void_p), _buf=buf)
 
 
+def host_shard(rank: int, nranks: int, allgather_bytes: Callable[[bytes], List[bytes]]) -> dict:
+    """comm_kind 3: the library bootstraps its peer-memory data plane through the caller's host
+    allgather (allgather_bytes(my_bytes) -> every rank's bytes in rank order), e.g. over a gloo
+    process group — so ranks may be separate processes sharing one GPU (CUDA IPC) or one GPU
+    each, without NCCL.  Plumbing only: byte marshalling for ipm_create's bootstrap."""
+
+    def cb(send, recv, nbytes, user):
+        try:
+            parts = allgather_bytes(C.string_at(send, nbytes))
+            if len(parts) != nranks or any(len(p) != nbytes for p in parts):
+                return 1
+            C.memmove(recv, b"".join(parts), nbytes * nranks)
+            return 0
+        except Exception:  # noqa: BLE001 — reported to the library as a failed allgather
+            return 1
+
+    fn = L.IPM_HOST_ALLGATHER(cb)
+    hc = L.ipm_host_comm(rank=rank, nranks=nranks, allgather=fn, user=None)
+    return dict(rank=rank, nranks=nranks, comm_kind=3, handle=C.cast(C.pointer(hc), C.c_void_p), _keep=(fn, hc))
+
+
+def torch_allgather_bytes(group=None) -> Callable[[bytes], List[bytes]]:
+    """allgather_bytes over a torch.distributed process group (any backend)."""
+    import torch.distributed as dist
+
+    def ag(b: bytes) -> List[bytes]:
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, b, group=group)
+        return out
+    return ag
+
+
 def create_nccl(tensors: dict, rank: int, nranks: int, **opts):
     """Collective over the default torch.distributed group: returns this rank's QP.
     tensors: the FULL problem except H, which must be this rank's row block."""
