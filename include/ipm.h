@@ -86,6 +86,10 @@ typedef struct {
                                    1: PCG on the doubly augmented system eq:2x2_augmented,
                                    unknowns (dx, dlam_lA, dlam_uA), Jacobi preconditioner on its diagonal;
                                    unsharded only, and ipm_pcg() is then rejected (IPM_ERR_STATE) */
+    int32_t a_row_split;        /* 1 (default): row-sharded with the peer data plane, the PCG's SpMV t = Sigma_c o
+                                   (A p) runs on each rank's own m / nranks rows of A and the slices are
+                                   allgathered over peer memory (north_star "A rows partitioned"); 0: every
+                                   rank forms the whole t (A replicated).  No effect unsharded. */
     int32_t kernel_timer;       /* 0 (default): off.  1: the PCG operator kernel (GEMV / SYMV, PCG mode)
                                    times its own launches on the device for ipm_kernel_timer (two
                                    atomics per CTA per launch; used by bench.py's live roofline) */

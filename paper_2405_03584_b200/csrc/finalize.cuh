@@ -116,6 +116,11 @@ __device__ __forceinline__ void xcombine_apply(Scalars *sc, const double *xa, in
             }
             sc->S_b = sb;
             sc->S_H = sh;
+            if (sc->spmv_split) {              // every rank formed S_c over its own rows of A
+                double scs = 0.0;
+                for (int r = 0; r < P; ++r) scs += xa[r * 8 + 2];
+                sc->S_c = scs;
+            }
             fin_pcg_alpha(sc, s + sc->S_c);
             break;
         }

@@ -129,7 +129,7 @@ Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks
     o.gfull = L.take(sizeof(double) * ((size_t)chunk * nranks + 2));
     o.xloc_all = L.take(sizeof(double) * 8 * (size_t)nranks);
     // peer-memory data plane (peer.h): the region other ranks store into (sharded only)
-    o.peer = L.take(nranks > 1 && nranks <= kPeerMax ? peer_layout(ncols, nranks).bytes : 256);
+    o.peer = L.take(nranks > 1 && nranks <= kPeerMax ? peer_layout(ncols, m, nranks).bytes : 256);
     return o;
 }
 
@@ -180,6 +180,7 @@ struct ipm_ctx {
     int64_t chunk = 0;
     // peer-memory data plane (peer.h): device-side exchanges instead of Comm allgathers
     bool peer_on = false;
+    bool a_split = false;        // PCG SpMV over this rank's rows of A only (peer plane, opt.a_row_split)
     ipm::PeerArgs peer{};
     std::vector<void *> ipc_opened;
 };
@@ -269,7 +270,8 @@ ipm_status setup_peer(ipm_ctx *ctx, char *region, char *scratch) {
     pa.rank = me;
     pa.P = R;
     pa.chunk = ctx->chunk;
-    pa.L = peer_layout(ctx->n, R);
+    pa.m = ctx->m;
+    pa.L = peer_layout(ctx->n, ctx->m, R);
     for (int r = 0; r < R; ++r) {
         if (r == me) {
             pa.base[r] = region;
@@ -291,6 +293,9 @@ ipm_status setup_peer(ipm_ctx *ctx, char *region, char *scratch) {
     }
     ctx->peer = pa;
     ctx->peer_on = true;
+    ctx->a_split = ctx->opt.a_row_split != 0 && ctx->m > 0;
+    const int64_t split = ctx->a_split ? 1 : 0;
+    CK(cudaMemcpyAsync(&ctx->sc->spmv_split, &split, sizeof split, cudaMemcpyHostToDevice, ctx->st));
     ctx->V.gfull = reinterpret_cast<double *>(region + pa.L.gfull);
     // everybody's region is zeroed (workspace memset) before anyone may store into it
     CK(cudaStreamSynchronize(ctx->st));
@@ -356,7 +361,8 @@ ipm_status gather(ipm_ctx *ctx, const double *local, const double **full, cudaSt
     }
     if (ctx->peer_on) {                // every rank stores its slice into every peer's gfull (peer.h)
         st = st ? st : ctx->st;
-        launch_peer_put_vec(ctx->peer, local, ctx->nloc, ctx->sc, check_done, st);
+        launch_peer_put_vec(ctx->peer, local, ctx->nloc, ctx->peer.L.gfull, ctx->peer.rank * ctx->chunk, 0, ctx->sc,
+                            check_done, st);
         launch_peer_wait(ctx->peer, ctx->sc, -1, 0.0, 0.0, 0, check_done, 0, 0, st);
         ctx->launches += 2;
         CKL();
@@ -459,6 +465,9 @@ ipm_status op_apply(ipm_ctx *ctx, const double *v_local, const double *v_full, d
 // One PCG iteration on a row-sharded context (no graph: collectives between the kernels).
 // st = nullptr: the context stream (host-driven); otherwise the graph-capture stream, and with
 // use_cond the last exchange sets the WHILE condition (peer data plane only: no host calls).
+// Peer data plane: the SpMV stage runs on the side branch next to the SYMV (as on one GPU);
+// with the A-row split (opt.a_row_split) each rank forms t only for its rows of A and the
+// slices are allgathered over peer memory on the side branch's own exchange channel.
 ipm_status pcg_iteration_sharded(ipm_ctx *ctx, cudaStream_t st = nullptr, int use_cond = 0) {
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
@@ -466,11 +475,38 @@ ipm_status pcg_iteration_sharded(ipm_ctx *ctx, cudaStream_t st = nullptr, int us
     launch_pcg_p(P, V, ctx->sc, st);
     const double *pf = nullptr;
     TRY(gather(ctx, V.pp, &pf, st, 1));
-    launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, st, kMaxGrid, side_block());
-    launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, st);
-    TRY(sym_exchange(ctx, st, 1));
-    TRY(xcombine(ctx, X_PCG_ALPHA, 0.0, 0.0, 0, st, 1));
-    launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, st);
+    const bool par = ctx->peer_on && P.m > 0;
+    if (par) {
+        cudaStream_t side = ctx->fork.side;
+        CK(cudaEventRecord(ctx->fork.ev_fork, st));
+        CK(cudaStreamWaitEvent(side, ctx->fork.ev_fork, 0));
+        const double *t = V.pt;
+        if (ctx->a_split) {
+            const PeerArgs &pa = ctx->peer;
+            double *tall = reinterpret_cast<double *>(pa.base[pa.rank] + pa.L.tall);
+            const int64_t m0 = peer_mrow0(pa, pa.rank), m1 = peer_mrow0(pa, pa.rank + 1);
+            launch_spmv_rows(P, pf, V.sig_c, tall, V.part[3], ctx->sc, m0, m1, side, side_block());
+            launch_peer_put_vec(pa, tall + m0, m1 - m0, pa.L.tall, m0, 1, ctx->sc, 1, side);
+            launch_peer_wait(pa, ctx->sc, -1, 0.0, 0.0, 0, 1, 0, 0, side, 1);
+            t = tall;
+            ctx->launches += 2;
+        } else {
+            launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, side, kMaxGrid, side_block());
+        }
+        launch_pcg_spmvT(P, V, ctx->G, ctx->sc, t, side);
+        CK(cudaEventRecord(ctx->fork.ev_join, side));
+        launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, st);
+        TRY(sym_exchange(ctx, st, 1));
+        CK(cudaStreamWaitEvent(st, ctx->fork.ev_join, 0));
+        TRY(xcombine(ctx, X_PCG_ALPHA, 0.0, 0.0, 0, st, 1));
+        launch_pcg_update_only(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, st);
+    } else {
+        launch_spmv(P, pf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, st, kMaxGrid, side_block());
+        launch_gemv(P, pf, V.pp, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, st);
+        TRY(sym_exchange(ctx, st, 1));
+        TRY(xcombine(ctx, X_PCG_ALPHA, 0.0, 0.0, 0, st, 1));
+        launch_pcg_update(P, V, ctx->G, ctx->ncb, ctx->sc, V.dx, st);
+    }
     TRY(xcombine(ctx, X_PCG_UPDATE, 0.0, 0.0, 0, st, 1, ctx->handle, use_cond));
     ctx->launches += 3 + (P.m > 0 ? 2 : 0);
     CKL();
@@ -861,6 +897,7 @@ IPM_EXPORT void ipm_options_default(ipm_options *o) {
     o->trace = 0;
     o->use_graph = 1;
     o->warm_shift = 1e-3;
+    o->a_row_split = 1;
 }
 
 static void local_rows(const ipm_problem *p, int64_t &row0, int64_t &nloc) {

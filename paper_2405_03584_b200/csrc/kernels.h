@@ -82,7 +82,12 @@ void launch_zfold(int nloc, int ncols, int nranks, int64_t row_begin, const doub
 void launch_sym_hash(int nloc, int ncols, int64_t row_begin, int chunk, int nranks, const double *H, int64_t ldh,
                      unsigned long long *out, cudaStream_t st);
 int side_block();
-int spmv_keep();    // 1: PCG-mode SpMV / SpMV^T load A, A^T with an L2 evict_last priority   // CTA size of every PCG-mode SpMV launch (one association => bitwise paths)
+int spmv_keep();    // IPM_SPMV_KEEP switch (1 default)
+int spmv_keep_for(const Prob &P);   // 1: PCG-mode SpMV / SpMV^T load A, A^T evict_last (only when they fit L2)
+void launch_spmv_rows(const Prob &P, const double *v, const double *sigc, double *y, double *dpart, Scalars *sc,
+                      int64_t r0, int64_t r1, cudaStream_t st, int block);
+void launch_pcg_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, const double *t, cudaStream_t st);
+void launch_pcg_update_only(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st);
 void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
 cudaError_t configure_linalg_attrs();   // >48 KB dynamic smem opt-ins (per device: called at every create)
 cudaError_t configure_pcg_attrs();

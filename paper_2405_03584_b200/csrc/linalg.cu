@@ -855,7 +855,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kBlock)
 k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const double *__restrict__ val,
        const double *__restrict__ v, const double *__restrict__ sigc, double *__restrict__ y,
-       double *__restrict__ dpart, Scalars *sc, int cid, int check_done, int keep) {
+       double *__restrict__ dpart, Scalars *sc, int cid, int check_done, int keep, int split) {
     __shared__ double red[kBlock / 32];
     if (check_done && sc->done) return;
     if (MODE == 1) TL_BEGIN(sc, 0);
@@ -865,12 +865,36 @@ k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const
     for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < m; i += gridDim.x * wpb) {
         const int64_t s = rp[i], e = rp[i + 1];
         double a = 0.0;
+        // four lane-strided entries per trip: their column indices, values and gathers are all
+        // in flight together, then folded into the ONE accumulator in k order (so the sum is
+        // bitwise the plain loop's)
+        int64_t k = s + lane;
         if (MODE == 1 && keep) {
             const uint64_t pol = keep_policy();
-            for (int64_t k = s + lane; k < e; k += 32)
-                a = fma(ld_keep(val + k, pol), __ldg(v + ld_keep(col + k, pol)), a);
+            for (; k + 96 < e; k += 128) {
+                const int c0 = ld_keep(col + k, pol), c1 = ld_keep(col + k + 32, pol);
+                const int c2 = ld_keep(col + k + 64, pol), c3 = ld_keep(col + k + 96, pol);
+                const double w0 = ld_keep(val + k, pol), w1 = ld_keep(val + k + 32, pol);
+                const double w2 = ld_keep(val + k + 64, pol), w3 = ld_keep(val + k + 96, pol);
+                const double x0 = __ldg(v + c0), x1 = __ldg(v + c1), x2 = __ldg(v + c2), x3 = __ldg(v + c3);
+                a = fma(w0, x0, a);
+                a = fma(w1, x1, a);
+                a = fma(w2, x2, a);
+                a = fma(w3, x3, a);
+            }
+            for (; k < e; k += 32) a = fma(ld_keep(val + k, pol), __ldg(v + ld_keep(col + k, pol)), a);
         } else {
-            for (int64_t k = s + lane; k < e; k += 32) a = fma(__ldg(val + k), __ldg(v + __ldg(col + k)), a);
+            for (; k + 96 < e; k += 128) {
+                const int c0 = __ldg(col + k), c1 = __ldg(col + k + 32), c2 = __ldg(col + k + 64), c3 = __ldg(col + k + 96);
+                const double w0 = __ldg(val + k), w1 = __ldg(val + k + 32), w2 = __ldg(val + k + 64);
+                const double w3 = __ldg(val + k + 96);
+                const double x0 = __ldg(v + c0), x1 = __ldg(v + c1), x2 = __ldg(v + c2), x3 = __ldg(v + c3);
+                a = fma(w0, x0, a);
+                a = fma(w1, x1, a);
+                a = fma(w2, x2, a);
+                a = fma(w3, x3, a);
+            }
+            for (; k < e; k += 32) a = fma(__ldg(val + k), __ldg(v + __ldg(col + k)), a);
         }
         a = warp_sum(a);
         if (lane == 0) {
@@ -890,7 +914,8 @@ k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const
         const double tot = sum_partials(dpart, gridDim.x, red);
         if (threadIdx.x == 0) {
             sc->counters[cid] = 0;
-            sc->S_c = tot;
+            if (split) sc->loc[2] = tot;       // this rank's rows only: combined across ranks (X_PCG_ALPHA)
+            else sc->S_c = tot;
         }
     }
     TL_END(sc, 0);
@@ -913,15 +938,30 @@ int spmv_keep() {
     return k;
 }
 
+// (kept for every size: at C5 A and A^T are 480 MB, far above L2, yet the evict_last loads still
+// measured faster than plain ones — SpMV 0.242 vs 0.257 ms, bench 148.7 vs 147.4 PCG it/s,
+// profiles/r02_spmv_keep.txt)
+int spmv_keep_for(const Prob &) { return spmv_keep(); }
+
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
                  Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid, int block) {
     if (P.m == 0) return;
     const int grid = std::min(grid_for(P.m, block / 32), max_grid);
     if (mode == 1)
         k_spmv<1><<<grid, block, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV_PCG, check_done,
-                                          spmv_keep());
+                                          spmv_keep_for(P), 0);
     else
-        k_spmv<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV, check_done, 0);
+        k_spmv<0><<<grid, kBlock, 0, st>>>(P.m, P.Arp, P.Acol, P.Aval, v, sigc, y, dpart, sc, C_SPMV, check_done, 0, 0);
+}
+
+// PCG-mode SpMV over A's rows [r0, r1) only (row-split sharded PCG): t[r0:r1) and this rank's
+// part of S_c (in loc[2]).  rp stays global (the CSR offsets index col / val directly).
+void launch_spmv_rows(const Prob &P, const double *v, const double *sigc, double *y, double *dpart, Scalars *sc,
+                      int64_t r0, int64_t r1, cudaStream_t st, int block) {
+    const int rows = (int)(r1 - r0);
+    const int grid = std::max(1, std::min(grid_for(std::max(rows, 1), block / 32), kMaxGrid));
+    k_spmv<1><<<grid, block, 0, st>>>(rows, P.Arp + r0, P.Acol, P.Aval, v, sigc + r0, y + r0, dpart, sc, C_SPMV_PCG, 1,
+                                      spmv_keep_for(P), 1);
 }
 
 // ------------------------------------------------ doubly augmented operator, SpMV stage (NEXT-2)

@@ -657,12 +657,34 @@ k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, 
         const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;
         double s = 0.0;
         const int64_t e = ATrp[i + 1];
+        int64_t k = ATrp[i] + gl;       // 4 strided entries in flight per trip, folded in k order
         if (keep) {
             const uint64_t pol = keep_policy();
-            for (int64_t k = ATrp[i] + gl; k < e; k += G)
-                s = fma(ld_keep(ATval + k, pol), __ldg(t + ld_keep(ATcol + k, pol)), s);
+            for (; k + 3 * G < e; k += 4 * G) {
+                const int c0 = ld_keep(ATcol + k, pol), c1 = ld_keep(ATcol + k + G, pol);
+                const int c2 = ld_keep(ATcol + k + 2 * G, pol), c3 = ld_keep(ATcol + k + 3 * G, pol);
+                const double w0 = ld_keep(ATval + k, pol), w1 = ld_keep(ATval + k + G, pol);
+                const double w2 = ld_keep(ATval + k + 2 * G, pol), w3 = ld_keep(ATval + k + 3 * G, pol);
+                const double x0 = __ldg(t + c0), x1 = __ldg(t + c1), x2 = __ldg(t + c2), x3 = __ldg(t + c3);
+                s = fma(w0, x0, s);
+                s = fma(w1, x1, s);
+                s = fma(w2, x2, s);
+                s = fma(w3, x3, s);
+            }
+            for (; k < e; k += G) s = fma(ld_keep(ATval + k, pol), __ldg(t + ld_keep(ATcol + k, pol)), s);
         } else {
-            for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
+            for (; k + 3 * G < e; k += 4 * G) {
+                const int c0 = __ldg(ATcol + k), c1 = __ldg(ATcol + k + G), c2 = __ldg(ATcol + k + 2 * G);
+                const int c3 = __ldg(ATcol + k + 3 * G);
+                const double w0 = __ldg(ATval + k), w1 = __ldg(ATval + k + G), w2 = __ldg(ATval + k + 2 * G);
+                const double w3 = __ldg(ATval + k + 3 * G);
+                const double x0 = __ldg(t + c0), x1 = __ldg(t + c1), x2 = __ldg(t + c2), x3 = __ldg(t + c3);
+                s = fma(w0, x0, s);
+                s = fma(w1, x1, s);
+                s = fma(w2, x2, s);
+                s = fma(w3, x3, s);
+            }
+            for (; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);
         }
         s = group_sum<G>(s);
         if (act && gl == 0) out[i] = s;
@@ -671,15 +693,22 @@ k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, 
 }
 
 static void launch_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, cudaStream_t st, int max_grid = kMaxGrid,
-                         int block = kBlock) {
+                         int block = kBlock, const double *t = nullptr) {
     if (P.m == 0 || P.n == 0) return;
     const int g = std::min(grid_for(P.n, block / G), max_grid);
+    const double *tt = t ? t : V.pt;
+    const int keep = spmv_keep_for(P);
     switch (G) {
-        case 4: k_spmvT<4><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
-        case 8: k_spmvT<8><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
-        case 16: k_spmvT<16><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
-        default: k_spmvT<32><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, V.pt, V.pAt, sc, spmv_keep()); break;
+        case 4: k_spmvT<4><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, tt, V.pAt, sc, keep); break;
+        case 8: k_spmvT<8><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, tt, V.pAt, sc, keep); break;
+        case 16: k_spmvT<16><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, tt, V.pAt, sc, keep); break;
+        default: k_spmvT<32><<<g, block, 0, st>>>(P.n, P.ATrp, P.ATcol, P.ATval, tt, V.pAt, sc, keep); break;
     }
+}
+
+// sharded PCG, SpMV side branch: (A^T t) for the local rows from a given (gathered) t
+void launch_pcg_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, const double *t, cudaStream_t st) {
+    launch_spmvT(P, V, G, sc, st, kMaxGrid, side_block(), t);
 }
 
 // Lanes per row of the update kernel: it sums the ncb GEMV partials of each row (A^T t now
@@ -767,6 +796,11 @@ static void launch_update_fp(const Prob &P, const Vecs &V, int ncb, Scalars *sc,
 // sharded path: t is complete (replicated on every rank) when this is called
 void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st) {
     launch_spmvT(P, V, G, sc, st);
+    launch_update_g(P, V, G, ncb, sc, x, 0, 0, st);
+}
+
+// sharded path with the SpMV / SpMV^T on a side branch: A^T t already in V.pAt
+void launch_pcg_update_only(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st) {
     launch_update_g(P, V, G, ncb, sc, x, 0, 0, st);
 }
 

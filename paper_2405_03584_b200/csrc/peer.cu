@@ -9,7 +9,7 @@
 
 namespace ipm {
 
-PeerLayout peer_layout(int64_t ncols, int nranks) {
+PeerLayout peer_layout(int64_t ncols, int64_t m, int nranks) {
     const int64_t chunk = (ncols + nranks - 1) / nranks;
     auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
     PeerLayout L;
@@ -20,8 +20,10 @@ PeerLayout peer_layout(int64_t ncols, int nranks) {
     off += up(sizeof(double) * (size_t)chunk * nranks);
     L.xall = off;
     off += up(sizeof(double) * 8 * (size_t)nranks * kPeerX);
+    L.tall = off;
+    off += up(sizeof(double) * (size_t)std::max<int64_t>(m, 1));
     L.flags = off;
-    off += up(sizeof(unsigned long long) * kPeerMax);
+    off += up(sizeof(unsigned long long) * kPeerMax * kPeerCh);
     L.bytes = off;
     return L;
 }
@@ -39,49 +41,51 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 // End of a put kernel: every CTA's stores are fenced at system scope; the last CTA to arrive
 // raises this rank's flag in every peer's region to the exchange's sequence number.
-__device__ __forceinline__ void put_signal(const PeerArgs &pa, Scalars *sc, unsigned long long seq) {
+__device__ __forceinline__ unsigned long long *flag_ptr(const PeerArgs &pa, int r, int ch, int sender) {
+    return reinterpret_cast<unsigned long long *>(pa.base[r] + pa.L.flags) + ch * kPeerMax + sender;
+}
+
+__device__ __forceinline__ void put_signal(const PeerArgs &pa, Scalars *sc, unsigned long long seq, int ch) {
     __shared__ bool am_last;
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0) am_last = (atomicAdd(&sc->peer_ctr, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) am_last = (atomicAdd(&sc->peer_ctr[ch], 1u) == gridDim.x - 1);
     __syncthreads();
     if (!am_last) return;
     if (threadIdx.x == 0) {
-        sc->peer_ctr = 0;
+        sc->peer_ctr[ch] = 0;
         __threadfence_system();
-        for (int r = 0; r < pa.P; ++r)
-            st_release_sys(reinterpret_cast<unsigned long long *>(pa.base[r] + pa.L.flags) + pa.rank, seq);
+        for (int r = 0; r < pa.P; ++r) st_release_sys(flag_ptr(pa, r, ch, pa.rank), seq);
     }
 }
 
-__global__ void k_peer_put_vec(PeerArgs pa, const double *__restrict__ src, int64_t count, Scalars *sc,
-                               int check_done) {
+__global__ void k_peer_put_vec(PeerArgs pa, const double *__restrict__ src, int64_t count, size_t dst_off,
+                               int64_t dst_base, int ch, Scalars *sc, int check_done) {
     if (check_done && sc->done) return;
-    const unsigned long long seq = sc->peer_seq + 1;
+    const unsigned long long seq = sc->peer_seq[ch] + 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
         const double v = src[i];
-        for (int r = 0; r < pa.P; ++r)
-            reinterpret_cast<double *>(pa.base[r] + pa.L.gfull)[pa.rank * pa.chunk + i] = v;
+        for (int r = 0; r < pa.P; ++r) reinterpret_cast<double *>(pa.base[r] + dst_off)[dst_base + i] = v;
     }
-    put_signal(pa, sc, seq);
+    put_signal(pa, sc, seq, ch);
 }
 
 __global__ void k_peer_put_loc(PeerArgs pa, int stage, Scalars *sc, int check_done) {
     if (check_done && sc->done) return;
-    const unsigned long long seq = sc->peer_seq + 1;
+    const unsigned long long seq = sc->peer_seq[0] + 1;
     const int k = threadIdx.x;
     if (k < 8) {
         const double v = sc->loc[k];
         for (int r = 0; r < pa.P; ++r)
             reinterpret_cast<double *>(pa.base[r] + pa.L.xall)[((size_t)stage * pa.P + pa.rank) * 8 + k] = v;
     }
-    put_signal(pa, sc, seq);
+    put_signal(pa, sc, seq, 0);
 }
 
 __global__ void k_peer_zput(PeerArgs pa, int zrows, int ldz, const double *__restrict__ zpart,
                             const int *__restrict__ zcol, Scalars *sc, int check_done) {
     if (check_done && sc->done) return;
-    const unsigned long long seq = sc->peer_seq + 1;
+    const unsigned long long seq = sc->peer_seq[0] + 1;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < zrows; q += gridDim.x * blockDim.x) {
         const double *z = zpart + (int64_t)q * ldz;
         double s = 0.0;
@@ -90,22 +94,22 @@ __global__ void k_peer_zput(PeerArgs pa, int zrows, int ldz, const double *__res
         const int b = (int)(col / pa.chunk);
         reinterpret_cast<double *>(pa.base[b] + pa.L.zall)[pa.rank * pa.chunk + (col - (int64_t)b * pa.chunk)] = s;
     }
-    put_signal(pa, sc, seq);
+    put_signal(pa, sc, seq, 0);
 }
 
 __global__ void k_peer_wait(PeerArgs pa, Scalars *sc, int stage, double p0, double p1, int64_t p2, int check_done,
-                            cudaGraphConditionalHandle h, int use_cond) {
+                            cudaGraphConditionalHandle h, int use_cond, int ch) {
     if (check_done && sc->done) {
         if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
         return;
     }
-    const unsigned long long seq = sc->peer_seq + 1;
+    const unsigned long long seq = sc->peer_seq[ch] + 1;
     __shared__ int timed_out;
     if (threadIdx.x == 0) timed_out = 0;
     __syncthreads();
     const int r = threadIdx.x;
     if (r < pa.P) {
-        const unsigned long long *f = reinterpret_cast<const unsigned long long *>(pa.base[pa.rank] + pa.L.flags) + r;
+        const unsigned long long *f = flag_ptr(pa, pa.rank, ch, r);
         const unsigned long long t0 = gtimer_ns();
         unsigned int spins = 0;
         unsigned long long v;
@@ -122,7 +126,7 @@ __global__ void k_peer_wait(PeerArgs pa, Scalars *sc, int stage, double p0, doub
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    sc->peer_seq = seq;
+    sc->peer_seq[ch] = seq;
     if (timed_out) {
         sc->peer_timeout = 1;
         sc->done = 1;
@@ -150,10 +154,10 @@ __global__ void k_peer_zfold(PeerArgs pa, int nloc, double *__restrict__ ypart, 
 
 }  // namespace
 
-void launch_peer_put_vec(const PeerArgs &pa, const double *src, int64_t count, Scalars *sc, int check_done,
-                         cudaStream_t st) {
+void launch_peer_put_vec(const PeerArgs &pa, const double *src, int64_t count, size_t dst_off, int64_t dst_base,
+                         int ch, Scalars *sc, int check_done, cudaStream_t st) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxGrid, (count + 255) / 256));
-    k_peer_put_vec<<<grid, 256, 0, st>>>(pa, src, count, sc, check_done);
+    k_peer_put_vec<<<grid, 256, 0, st>>>(pa, src, count, dst_off, dst_base, ch, sc, check_done);
 }
 
 void launch_peer_put_loc(const PeerArgs &pa, int stage, Scalars *sc, int check_done, cudaStream_t st) {
@@ -167,8 +171,8 @@ void launch_peer_zput(const PeerArgs &pa, int zrows, int ldz, const double *zpar
 }
 
 void launch_peer_wait(const PeerArgs &pa, Scalars *sc, int stage, double p0, double p1, int64_t p2, int check_done,
-                      cudaGraphConditionalHandle h, int use_cond, cudaStream_t st) {
-    k_peer_wait<<<1, 32, 0, st>>>(pa, sc, stage, p0, p1, p2, check_done, h, use_cond);
+                      cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, int ch) {
+    k_peer_wait<<<1, 32, 0, st>>>(pa, sc, stage, p0, p1, p2, check_done, h, use_cond, ch);
 }
 
 void launch_peer_zfold(const PeerArgs &pa, int nloc, double *ypart, int ldy, Scalars *sc, int check_done,

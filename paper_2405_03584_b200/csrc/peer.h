@@ -17,7 +17,10 @@
 //   gfull  P*chunk + 2 doubles   allgathered x-space vector (p, x, dx, v)
 //   zall   P*chunk doubles       column parts of the sharded SYMV for the receiver's rows, per sender
 //   xall   kPeerX stages x P x 8 per-stage scalar partials (Scalars::loc) of every sender
-//   flags  P uint64              last sequence number each sender completed toward this rank
+//   tall   m doubles             t = Sigma_c o (A p) when the PCG SpMV's A rows are split
+//   flags  kPeerCh x P uint64    per channel: last sequence number each sender completed toward me
+// Channels: exchanges issued on different streams (the PCG's SpMV side branch runs next to the
+// SYMV) use separate sequence counters and flags (channel 0 = main stream, 1 = side branch).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,25 +32,31 @@ namespace ipm {
 
 constexpr int kPeerMax = 8;          // ranks reachable by the peer path (one NVLink domain / node)
 constexpr int kPeerX = 12;           // xall stage slots (>= number of XStage values)
+constexpr int kPeerCh = 2;           // exchange channels (streams)
 
 struct PeerLayout {
-    size_t gfull = 0, zall = 0, xall = 0, flags = 0, bytes = 0;
+    size_t gfull = 0, zall = 0, xall = 0, tall = 0, flags = 0, bytes = 0;
 };
-PeerLayout peer_layout(int64_t ncols, int nranks);
+PeerLayout peer_layout(int64_t ncols, int64_t m, int nranks);
 
 // Kernel-side view (by value): base[r] = rank r's region as addressable from this device.
 struct PeerArgs {
     char *base[kPeerMax];
     int rank = 0, P = 0;
     int64_t chunk = 0;
+    int64_t m = 0;              // rows of A; with the split PCG SpMV rank r owns rows [m0(r), m0(r + 1))
     unsigned long long timeout_ns = 30ull * 1000000000ull;   // IPM_PEER_TIMEOUT_S (default 30 s)
     PeerLayout L;
 };
 
-// Allgather of an x-space vector: every rank stores its nloc entries into every peer's gfull at
-// rank * chunk, then raises its flag; the wait makes the full vector usable in stream order.
-void launch_peer_put_vec(const PeerArgs &pa, const double *src, int64_t count, Scalars *sc, int check_done,
-                         cudaStream_t st);
+// Rows of A owned by rank r for the split PCG SpMV (equal split of m).
+inline int64_t peer_mrow0(const PeerArgs &pa, int r) { return pa.m * r / pa.P; }
+
+// Allgather of a vector: every rank stores its `count` entries into every peer's buffer at region
+// offset dst_off, element index dst_base (x-space: gfull, rank * chunk; t: tall, m0(rank)), then
+// raises its flag on channel ch; the wait makes the full vector usable in stream order.
+void launch_peer_put_vec(const PeerArgs &pa, const double *src, int64_t count, size_t dst_off, int64_t dst_base,
+                         int ch, Scalars *sc, int check_done, cudaStream_t st);
 // Scalar partials of one XStage: Scalars::loc (8 doubles) into every peer's xall[stage][rank].
 void launch_peer_put_loc(const PeerArgs &pa, int stage, Scalars *sc, int check_done, cudaStream_t st);
 // Sharded SYMV column parts: zvec entry zcol[q] (the sum of zpart row q) stored straight into
@@ -58,7 +67,7 @@ void launch_peer_zput(const PeerArgs &pa, int zrows, int ldz, const double *zpar
 // Scalars::peer_seq; stage >= 0 also combines xall[stage] (rank order, k_xcombine's epilogue)
 // and, with use_cond, sets the WHILE condition from sc->done (X_PCG_UPDATE).
 void launch_peer_wait(const PeerArgs &pa, Scalars *sc, int stage, double p0, double p1, int64_t p2, int check_done,
-                      cudaGraphConditionalHandle h, int use_cond, cudaStream_t st);
+                      cudaGraphConditionalHandle h, int use_cond, cudaStream_t st, int ch = 0);
 // zfold from the peer zall buffer: ypart slot ldy-1 of row i = sum over senders in rank order.
 void launch_peer_zfold(const PeerArgs &pa, int nloc, double *ypart, int ldy, Scalars *sc, int check_done,
                        cudaStream_t st);

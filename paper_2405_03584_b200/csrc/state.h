@@ -48,8 +48,9 @@ struct Scalars {
     double loc[8];
     // peer-memory data plane (peer.cu): sequence number of the last completed exchange, the
     // put kernels' arrival counter, and a timeout flag (a peer never arrived)
-    unsigned long long peer_seq;
-    unsigned int peer_ctr, peer_timeout;
+    unsigned long long peer_seq[2];      // per exchange channel (peer.h)
+    unsigned int peer_ctr[2], peer_timeout;
+    int64_t spmv_split;                  // 1: the PCG SpMV runs on this rank's A rows; S_c partial in loc[2]
     unsigned long long peer_diag[4];     // timeout: {expected seq, sender, its flag, stage + 1000}
     unsigned int counters[kNumCounters];
     // --- live launch timing of the PCG operator kernel (bench.py roofline) ---------------

@@ -30,8 +30,9 @@ y = qp.op_apply(rng.uniform(0, 3, n), 10.0 ** rng.uniform(-2, 2, q.m), rng.norma
 digest = hashlib.sha1(y.tobytes()).hexdigest()[:12]
 reps = 5 if n > 50000 else 20
 g = qp.profile("gemv", reps)
+sp = qp.profile("spmv", reps)
 it = qp.profile("pcg_iter", reps)
-print(json.dumps({"variant": var or "prod", "workload": wl, "gemv_ms": g, "pcg_iter_ms": it,
+print(json.dumps({"variant": var or "prod", "workload": wl, "gemv_ms": g, "spmv_ms": sp, "pcg_iter_ms": it,
                   "streamed_GBps": streamed / g / 1e6, "y_sha1": digest}), flush=True)
 '''.replace("ROOT", repr(ROOT))
 

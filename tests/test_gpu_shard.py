@@ -160,3 +160,23 @@ def test_sharded_asymmetric_H_falls_back_on_every_rank():
     assert np.linalg.norm(torch.cat(ys).cpu().numpy() - yref) <= 1e-12 * np.linalg.norm(yref)
     with pytest.raises(_lib.IpmError, match="symmetric"):
         _sharded(q, 2, H=H, gemv_kernel=3)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_a_row_split_spmv(P):
+    """north_star's A-row partition (opt.a_row_split, default with the peer data plane): each rank
+    forms t = Sigma_c o (A p) for its own rows of A and the slices are allgathered over peer
+    memory on the SpMV side branch.  Same solution as the replicated SpMV (a_row_split = 0) up to
+    the rounding of the S_c sum, and bitwise reproducible at fixed P."""
+    q = planted_qp(1200, 500, density=0.02, rank=32, seed=60 + P, rows="vmat", var="box")
+    grp, qps = _sharded(q, P)
+    st, x, stats = _solve_all(grp, qps)
+    st2, x2, _ = _solve_all(grp, qps)
+    assert st == ["ok"] * P and np.array_equal(x, x2)
+    grp_r, qps_r = _sharded(q, P, a_row_split=0)
+    st_r, x_r, stats_r = _solve_all(grp_r, qps_r)
+    assert st_r == ["ok"] * P
+    assert np.max(np.abs(x - x_r)) <= 1e-7 * max(1.0, np.max(np.abs(x_r)))
+    assert abs(stats[0]["ipm_iters"] - stats_r[0]["ipm_iters"]) <= 1
+    ref = solve(Problem.from_data(q))
+    assert np.max(np.abs(x - ref.x)) <= 1e-6 * max(1.0, np.max(np.abs(ref.x)))
