@@ -45,6 +45,7 @@ __device__ __forceinline__ double group_sum(double v) {
 __device__ __forceinline__ double block_sum(double v, double *sh) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     v = warp_sum(v);
+    __syncwarp();                             // reconverged warp at the barrier (synccheck)
     __syncthreads();
     if (lane == 0) sh[wid] = v;
     __syncthreads();
@@ -56,6 +57,7 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 __device__ __forceinline__ double block_min(double v, double *sh) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     v = warp_min(v);
+    __syncwarp();
     __syncthreads();
     if (lane == 0) sh[wid] = v;
     __syncthreads();
@@ -67,6 +69,7 @@ __device__ __forceinline__ double block_min(double v, double *sh) {
 __device__ __forceinline__ double block_max(double v, double *sh) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     v = warp_max(v);
+    __syncwarp();
     __syncthreads();
     if (lane == 0) sh[wid] = v;
     __syncthreads();
@@ -82,6 +85,7 @@ __device__ __forceinline__ double block_max(double v, double *sh) {
 __device__ __forceinline__ bool last_block(unsigned int *counter) {
     __shared__ bool am_last;
     __threadfence();
+    __syncwarp();
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned int prev = atomicAdd(counter, 1u);
