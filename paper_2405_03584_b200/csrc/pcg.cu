@@ -510,32 +510,16 @@ __device__ __forceinline__ void block_sum2(double &a, double &b, double *sh) {
     b = tb;
 }
 
-__global__ void __launch_bounds__(kSmallThreads)
-k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_t *__restrict__ Arp,
-            const int *__restrict__ Acol, const double *__restrict__ Aval, const int64_t *__restrict__ ATrp,
-            const int *__restrict__ ATcol, const double *__restrict__ ATval, const double *__restrict__ sigb,
-            const double *__restrict__ sigc, const double *__restrict__ Minv, double *x, double *r, double *z,
-            double *p, double *t, double *y, Scalars *sc, int t_in_smem, int h_in_smem) {
-    __shared__ double red[64];
-    extern __shared__ __align__(16) double sm[];
-    if (sc->done) return;
+// The loop of k_pcg_small, templated on the index type of the staged / global CSR arrays.
+template <typename RP>
+__device__ __forceinline__ void pcg_small_loop(int n, int m, const double *Hs, int64_t ldhs, const RP *Arp,
+                                               const int *Acol, const double *Aval, const RP *ATrp, const int *ATcol,
+                                               const double *ATval, const double *sigc, double *sp, double *sr,
+                                               double *sz, double *sx, double *sy, const double *sM,
+                                               const double *sb, double *st, double *x, double *r, double *z,
+                                               double *p, double *t, double *y, Scalars *sc, int t_in_smem,
+                                               double *red) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    double *sp = sm, *sr = sm + n, *sz = sm + 2 * n, *sx = sm + 3 * n, *sy = sm + 4 * n, *sM = sm + 5 * n,
-           *sb = sm + 6 * n;
-    double *st = t_in_smem ? sm + 7 * n : t;
-    double *sH = sm + 7 * n + (t_in_smem ? m : 0);
-    const double *Hs = h_in_smem ? sH : H;
-    const int64_t ldhs = h_in_smem ? n : ldh;
-    for (int i = tid; i < n; i += blockDim.x) {
-        sp[i] = p[i];
-        sr[i] = r[i];
-        sz[i] = z[i];
-        sx[i] = x[i];
-        sM[i] = Minv[i];
-        sb[i] = sigb[i];
-    }
-    if (h_in_smem)
-        for (int64_t e = tid; e < (int64_t)n * n; e += blockDim.x) sH[e] = H[(e / n) * ldh + e % n];
     double rho = sc->rho, rho_old = sc->rho_old, rr = sc->rr, pkp = 0.0, alpha_last = 0.0;
     int64_t it = sc->it, it_rs = sc->it_rs;
     const double tol2 = sc->tol2;
@@ -620,6 +604,59 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
     }
 }
 
+__global__ void __launch_bounds__(kSmallThreads)
+k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_t *__restrict__ Arp,
+            const int *__restrict__ Acol, const double *__restrict__ Aval, const int64_t *__restrict__ ATrp,
+            const int *__restrict__ ATcol, const double *__restrict__ ATval, const double *__restrict__ sigb,
+            const double *__restrict__ sigc, const double *__restrict__ Minv, double *x, double *r, double *z,
+            double *p, double *t, double *y, Scalars *sc, int t_in_smem, int h_in_smem, int a_in_smem,
+            int64_t nnz) {
+    __shared__ double red[64];
+    extern __shared__ __align__(16) double sm[];
+    if (sc->done) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    double *sp = sm, *sr = sm + n, *sz = sm + 2 * n, *sx = sm + 3 * n, *sy = sm + 4 * n, *sM = sm + 5 * n,
+           *sb = sm + 6 * n;
+    double *st = t_in_smem ? sm + 7 * n : t;
+    double *sH = sm + 7 * n + (t_in_smem ? m : 0);
+    const double *Hs = h_in_smem ? sH : H;
+    const int64_t ldhs = h_in_smem ? n : ldh;
+    for (int i = tid; i < n; i += blockDim.x) {
+        sp[i] = p[i];
+        sr[i] = r[i];
+        sz[i] = z[i];
+        sx[i] = x[i];
+        sM[i] = Minv[i];
+        sb[i] = sigb[i];
+    }
+    if (h_in_smem)
+        for (int64_t e = tid; e < (int64_t)n * n; e += blockDim.x) sH[e] = H[(e / n) * ldh + e % n];
+    // A, A^T (CSR, int32 offsets) and sigma_c staged in shared memory too when they fit: every
+    // phase then runs at shared-memory latency (same loops, same association: bitwise unchanged)
+    if (a_in_smem) {
+        double *sc_ = sH + (h_in_smem ? (int64_t)n * n : 0);
+        double *aval = sc_ + m, *atval = aval + nnz;
+        int *arp = reinterpret_cast<int *>(atval + nnz), *acol = arp + (m + 1), *atrp = acol + nnz,
+            *atcol = atrp + (n + 1);
+        for (int i = tid; i < m; i += blockDim.x) sc_[i] = sigc[i];
+        for (int i = tid; i <= m; i += blockDim.x) arp[i] = (int)Arp[i];
+        for (int i = tid; i <= n; i += blockDim.x) atrp[i] = (int)ATrp[i];
+        for (int64_t k = tid; k < nnz; k += blockDim.x) {
+            aval[k] = Aval[k];
+            acol[k] = Acol[k];
+            atval[k] = ATval[k];
+            atcol[k] = ATcol[k];
+        }
+        __syncthreads();
+        pcg_small_loop(n, m, Hs, ldhs, arp, acol, aval, atrp, atcol, atval, sc_, sp, sr, sz, sx, sy, sM, sb, st, x, r,
+                       z, p, t, y, sc, t_in_smem, red);
+    } else {
+        pcg_small_loop(n, m, Hs, ldhs, Arp, Acol, Aval, ATrp, ATcol, ATval, sigc, sp, sr, sz, sx, sy, sM, sb, st, x, r,
+                       z, p, t, y, sc, t_in_smem, red);
+    }
+}
+
+
 cudaError_t configure_pcg_attrs() {
     return cudaFuncSetAttribute(k_pcg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
 }
@@ -630,9 +667,13 @@ void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cuda
     if (t_in) bytes += (size_t)P.m * 8;
     const int h_in = (bytes + (size_t)P.n * P.n * 8 <= kSmallSmemMax) ? 1 : 0;
     if (h_in) bytes += (size_t)P.n * P.n * 8;
+    // sigma_c + A and A^T values (8 B) + int32 row offsets and columns (4 B)
+    const size_t abytes = 8 * ((size_t)P.m + 2 * (size_t)P.nnz) + 4 * ((size_t)P.m + 1 + (size_t)P.n + 1 + 2 * (size_t)P.nnz);
+    const int a_in = (P.m > 0 && bytes + abytes <= kSmallSmemMax) ? 1 : 0;
+    if (a_in) bytes += abytes;
     k_pcg_small<<<1, kSmallThreads, bytes, st>>>(P.n, P.m, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol,
                                                  P.ATval, V.sig_b, V.sig_c, V.Minv, x, V.pr, V.pz, V.pp, V.pt, V.py,
-                                                 sc, t_in, h_in);
+                                                 sc, t_in, h_in, a_in, P.nnz);
 }
 
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {

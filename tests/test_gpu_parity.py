@@ -262,21 +262,38 @@ def test_host_loop_fallback_equals_graph():
     assert torch.equal(a.solution()["x"], b.solution()["x"])
 
 
-def test_single_cta_pcg_small_n():
+@pytest.mark.parametrize("shape", ["C1", "h_global", "t_global"])
+def test_single_cta_pcg_small_n(shape):
     """n <= 256: the whole PCG loop in one CTA (launch-latency path) agrees with the
-    multi-kernel host loop to rounding and with the oracle."""
-    q = config("C1", 6)
+    multi-kernel host loop to rounding and with the oracle — with everything staged in shared
+    memory (C1), with H read from global memory (n = 200: 320 KB > the 200 KB budget) and with
+    t and A in global memory (n = 64, m = 30000)."""
+    if shape == "C1":
+        q = config("C1", 6)
+    elif shape == "h_global":
+        q = planted_qp(200, 50, density=0.1, rank=64, seed=6, rows="mixed", var="mixed")
+    else:   # m >> n: no well-posed planted QP, so only the PCG hook runs on it
+        q = planted_qp(64, 30000, density=0.05, rank=32, seed=7, rows="mixed", var="mixed")
     a = _qp(q)               # single-CTA PCG
     b = _qp(q, use_graph=0)  # multi-kernel loop
-    assert a.solve() == "ok" and b.solve() == "ok"
-    xa, xb = a.solution()["x"].cpu().numpy(), b.solution()["x"].cpu().numpy()
-    assert np.max(np.abs(xa - xb)) <= 1e-9 * max(1.0, np.max(np.abs(xb)))
-    assert abs(a.stats()["ipm_iters"] - b.stats()["ipm_iters"]) <= 1
+    if shape != "t_global":
+        assert a.solve() == "ok" and b.solve() == "ok"
+        xa, xb = a.solution()["x"].cpu().numpy(), b.solution()["x"].cpu().numpy()
+        assert np.max(np.abs(xa - xb)) <= 1e-9 * max(1.0, np.max(np.abs(xb)))
+        assert abs(a.stats()["ipm_iters"] - b.stats()["ipm_iters"]) <= 1
     sb, sc, _ = _rand_sigmas(q, 9)
+    sc = np.minimum(sc, 10.0)
     K = okkt.condensed_matrix(q.H, q.A_dense(), sb, sc)
     rhs = np.random.default_rng(2).normal(size=q.n)
     x, it = a.pcg(sb, sc, rhs, 1e-11)
     assert np.linalg.norm(rhs - K @ x.cpu().numpy()) <= 1.0000001e-11 * np.linalg.norm(rhs)
+    xb_, itb = b.pcg(sb, sc, rhs, 1e-11)
+    assert np.max(np.abs(x.cpu().numpy() - xb_.cpu().numpy())) <= 1e-8 * np.max(np.abs(xb_.cpu().numpy()))
+    # the k-step recurrence of the single-CTA loop against the textbook PCG (oracle.pcg)
+    from oracle.pcg import pcg as oracle_pcg
+    ref = oracle_pcg(lambda v: K @ v, 1.0 / np.diag(K), rhs, maxit=4)
+    out = a.pcg_iterate(sb, sc, rhs, 4)
+    assert np.max(np.abs(out["x"].cpu().numpy() - ref.x)) <= 1e-11 * np.max(np.abs(ref.x))
 
 
 # ---------------------------------------------------------------- validation / errors
