@@ -240,6 +240,12 @@ ipm_status ipm_set_linear_term(ipm_ctx *ctx, const double *g);
 ipm_status ipm_update_hessian_rank2(ipm_ctx *ctx, const double *u, double alpha,
                                     const double *v, double beta);
 ipm_status ipm_warm_start(ipm_ctx *ctx);
+/* Replace the QP's bounds (device, FULL length even when sharded; copied).  In the paper's SQP
+ * every sub-problem's linearised constraints g(x_k) + grad g(x_k)^T d <= 0 shift with the iterate
+ * (P:140-146), so a sequence of QPs changes its bounds as well as g and H.  Validated like
+ * ipm_create (NaN, l < u); which entries are finite may not change (it fixes the bound families),
+ * else IPM_ERR_INVALID and nothing is changed.  Synchronises the context stream. */
+ipm_status ipm_set_bounds(ipm_ctx *ctx, const double *l, const double *u, const double *xl, const double *xu);
 
 /* Replace / read the iterate (masked full-length layout; order lA, uA, lx, ux). */
 ipm_status ipm_set_iterate(ipm_ctx *ctx, const double *x, const double *const s4[4],

@@ -120,6 +120,7 @@ _sigs = {
     "ipm_op_apply": ([_P, _P, _P, _P, _P], _S),
     "ipm_op_diag": ([_P, _P, _P, _P], _S),
     "ipm_pcg": ([_P, _P, _P, _P, _P, _D, C.POINTER(C.c_int32)], _S),
+    "ipm_set_bounds": ([_P, _P, _P, _P, _P], _S),
     "ipm_pcg_iterate": ([_P, _P, _P, _P, C.c_int32, _P, _P, _P, _P, C.POINTER(_D)], _S),
     "ipm_profile": ([_P, C.c_int32, C.c_int32, C.POINTER(_D)], _S),
     "ipm_kernel_launches": ([_P], C.c_int64),

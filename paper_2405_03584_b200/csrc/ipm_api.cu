@@ -1329,6 +1329,44 @@ IPM_EXPORT ipm_status ipm_set_linear_term(ipm_ctx *ctx, const double *g) {
     return IPM_OK;
 }
 
+IPM_EXPORT ipm_status ipm_set_bounds(ipm_ctx *ctx, const double *l, const double *u, const double *xl,
+                                     const double *xu) {
+    if (!ctx || !xl || !xu || (ctx->m > 0 && (!l || !u))) return fail(ctx, IPM_ERR_INVALID, "null argument");
+    const int64_t m = ctx->m, n = ctx->n;
+    std::vector<double> hl(m), hu(m), hxl(n), hxu(n), ol(m), ou(m), oxl(ctx->nloc), oxu(ctx->nloc);
+    CK(cudaStreamSynchronize(ctx->st));
+    if (m > 0) {
+        CK(cudaMemcpy(hl.data(), l, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hu.data(), u, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ol.data(), ctx->P.l, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ou.data(), ctx->P.u, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    }
+    CK(cudaMemcpy(hxl.data(), xl, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hxu.data(), xu, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(oxl.data(), ctx->P.xl, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(oxu.data(), ctx->P.xu, sizeof(double) * ctx->nloc, cudaMemcpyDeviceToHost));
+    TRY(check_bounds(ctx, hl, hu, "row"));
+    TRY(check_bounds(ctx, hxl, hxu, "variable"));
+    // the finite pattern fixes the bound families (masks, #bounds, mu0): it may not change
+    for (int64_t i = 0; i < m; ++i)
+        if (std::isfinite(hl[i]) != std::isfinite(ol[i]) || std::isfinite(hu[i]) != std::isfinite(ou[i]))
+            return fail(ctx, IPM_ERR_INVALID, "row %lld: which bounds are finite may not change", (long long)i);
+    for (int64_t j = 0; j < ctx->nloc; ++j)
+        if (std::isfinite(hxl[ctx->row0 + j]) != std::isfinite(oxl[j]) ||
+            std::isfinite(hxu[ctx->row0 + j]) != std::isfinite(oxu[j]))
+            return fail(ctx, IPM_ERR_INVALID, "variable %lld: which bounds are finite may not change",
+                        (long long)(ctx->row0 + j));
+    if (m > 0) {
+        CK(cudaMemcpyAsync(const_cast<double *>(ctx->P.l), l, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->st));
+        CK(cudaMemcpyAsync(const_cast<double *>(ctx->P.u), u, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    CK(cudaMemcpyAsync(const_cast<double *>(ctx->P.xl), xl + ctx->row0, sizeof(double) * ctx->nloc,
+                       cudaMemcpyDeviceToDevice, ctx->st));
+    CK(cudaMemcpyAsync(const_cast<double *>(ctx->P.xu), xu + ctx->row0, sizeof(double) * ctx->nloc,
+                       cudaMemcpyDeviceToDevice, ctx->st));
+    return IPM_OK;
+}
+
 IPM_EXPORT ipm_status ipm_update_hessian_rank2(ipm_ctx *ctx, const double *u, double alpha, const double *v,
                                                double beta) {
     if (!ctx || !u || !v) return fail(ctx, IPM_ERR_INVALID, "null argument");

@@ -209,6 +209,11 @@ class QP:
         L.check(L.ipm_update_hessian_rank2(self.ctx, _ptr(uu), float(alpha), _ptr(vv), float(beta)), self.ctx)
         self.stream.synchronize()
 
+    def set_bounds(self, l, u, xl, xu):
+        """New bounds for the next solve (same finite pattern; ipm_set_bounds)."""
+        self._bounds_new = [_dev(a, torch.float64, self.device) for a in (l, u, xl, xu)]
+        L.check(L.ipm_set_bounds(self.ctx, *[_ptr(a) for a in self._bounds_new]), self.ctx)
+
     def warm_start(self):
         L.check(L.ipm_warm_start(self.ctx), self.ctx)
 

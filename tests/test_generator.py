@@ -61,8 +61,8 @@ def test_generator_is_pure():
 
 
 def test_c4_sequence_stays_planted():
-    """after every BFGS rank-2 update of H the planted formula re-derives g_k,
-    so the planted x* is the exact optimum of each QP of the sequence — checked by the oracle
+    """after every BFGS rank-2 update of H, the random walk of x* (5 % active-set
+    flips) re-plants the row bounds and g_k, so x*_k is the exact optimum of each QP of the sequence — checked by the oracle
     (x* and f*_k within its duality-gap error)."""
     from gen.sqp_sequence import sqp_sequence
     from oracle.bfgs import rank2_update
@@ -72,7 +72,7 @@ def test_c4_sequence_stays_planted():
     H = q.H.copy()
     for up in ups:
         H = rank2_update(H, up.u, up.alpha, up.v, up.beta)
-        r = solve(Problem(H=H, g=up.g.copy(), A=q.A_scipy(), l=q.l, u=q.u, xl=q.xl, xu=q.xu))
+        r = solve(Problem(H=H, g=up.g.copy(), A=q.A_scipy(), l=up.l, u=up.ub, xl=q.xl, xu=q.xu))
         assert r.status == "converged"
-        assert np.max(np.abs(r.x - q.x_star)) <= 1e-6
+        assert np.max(np.abs(r.x - up.x_star)) <= 1e-6
         assert abs(r.obj - up.f_star) <= 1e-8 * abs(up.f_star)

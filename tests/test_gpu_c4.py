@@ -60,15 +60,39 @@ def test_sqp_sequence_warm_start_matches_oracle(seed):
     for k, up in enumerate(ups):
         qp.update_hessian_rank2(up.u, up.alpha, up.v, up.beta)
         qp.set_linear_term(up.g)
+        qp.set_bounds(up.l, up.ub, q.xl, q.xu)
         qp.warm_start()
         assert qp.solve() == "ok"
         sol = qp.solution()
         st = qp.stats()
         H = rank2_update(H, up.u, up.alpha, up.v, up.beta)
-        p = Problem(H=H, g=up.g.copy(), A=q.A_scipy(), l=q.l, u=q.u, xl=q.xl, xu=q.xu)
+        p = Problem(H=H, g=up.g.copy(), A=q.A_scipy(), l=up.l, u=up.ub, xl=q.xl, xu=q.xu)
         ref = solve(p, Options(), start=warm_start_point(p, ref.x, ref.it.lam, Options()))
         assert ref.status == "converged"
         x = sol["x"].cpu().numpy()
         assert np.max(np.abs(x - ref.x)) <= 1e-6 * max(1.0, np.max(np.abs(ref.x))), k
         assert abs(sol["obj"] - ref.obj) <= 1e-8 * max(1.0, abs(ref.obj)), k
         assert abs(st["ipm_iters"] - ref.iters) <= 2, (k, st["ipm_iters"], ref.iters)
+
+
+def test_set_bounds_validation():
+    """ipm_set_bounds: new values accepted; a change of which bounds are finite, NaN or l >= u
+    rejected with nothing changed (include/ipm.h)."""
+    from paper_2405_03584_b200 import QP
+    from paper_2405_03584_b200._lib import IpmError
+    q = planted_qp(400, 100, density=0.05, rank=16, seed=5, rows="vmat", var="box")
+    qp = QP(device=DEV, **problem_tensors(q, DEV))
+    assert qp.solve() == "ok"
+    l2, u2 = q.l - 0.01 * np.isfinite(q.l), q.u + 0.01 * np.isfinite(q.u)
+    qp.set_bounds(l2, u2, q.xl, q.xu)
+    ref = solve(Problem(H=q.H, g=q.g, A=q.A_scipy(), l=l2, u=u2, xl=q.xl, xu=q.xu))
+    assert qp.solve() == "ok"
+    assert np.max(np.abs(qp.solution()["x"].cpu().numpy() - ref.x)) <= 1e-6
+    bad = l2.copy()
+    bad[np.flatnonzero(np.isfinite(bad))[0]] = -np.inf
+    with pytest.raises(IpmError):
+        qp.set_bounds(bad, u2, q.xl, q.xu)
+    bad = q.xu.copy()
+    bad[0] = q.xl[0]
+    with pytest.raises(IpmError):
+        qp.set_bounds(l2, u2, q.xl, bad)
