@@ -90,6 +90,11 @@ typedef struct {
                                    (A p) runs on each rank's own m / nranks rows of A and the slices are
                                    allgathered over peer memory (north_star "A rows partitioned"); 0: every
                                    rank forms the whole t (A replicated).  No effect unsharded. */
+    int32_t pcg_single_reduction; /* row-sharded only.  0 (default): Jacobi PCG with two scalar exchanges per
+                                   iteration (p^T K p, then r^T z / ||r||^2).  1: the Chronopoulos-Gear
+                                   single-reduction form — the operator is applied to u = M^-1 r and one
+                                   exchange carries u^T K u, r^T u and ||r||^2 (same iterates in exact
+                                   arithmetic; one extra operator apply at the end of each solve) */
     int32_t kernel_timer;       /* 0 (default): off.  1: the PCG operator kernel (GEMV / SYMV, PCG mode)
                                    times its own launches on the device for ipm_kernel_timer (two
                                    atomics per CTA per launch; used by bench.py's live roofline) */

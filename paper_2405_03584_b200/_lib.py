@@ -31,7 +31,8 @@ class ipm_options(C.Structure):
                 ("pcg_rtol_floor", C.c_double), ("pcg_atol", C.c_double), ("pcg_max_iter", C.c_int32),
                 ("predictor_corrector", C.c_int32), ("trace", C.c_int32), ("use_graph", C.c_int32),
                 ("warm_shift", C.c_double), ("gemv_kernel", C.c_int32), ("pcg_warm_start", C.c_int32),
-                ("pcg_system", C.c_int32), ("a_row_split", C.c_int32), ("kernel_timer", C.c_int32)]
+                ("pcg_system", C.c_int32), ("a_row_split", C.c_int32), ("pcg_single_reduction", C.c_int32),
+                ("kernel_timer", C.c_int32)]
 
 
 class ipm_problem(C.Structure):

@@ -147,6 +147,53 @@ __device__ __forceinline__ void xcombine_apply(Scalars *sc, const double *xa, in
         case X_MUAFF:
             sc->muaff = sc->muaff_m + sum(5);
             break;
+        case X_CG: {
+            // Chronopoulos-Gear PCG (one reduction per iteration): loc = {S_b, S_H, S_c part,
+            // gamma = r^T u, ||r||^2} of the current u = M^-1 r and w = K u.  Stop before the
+            // update when ||r||^2 <= tol^2 or the cap is reached; else
+            //   beta = gamma / gamma_prev,  alpha = gamma / (delta - beta gamma / alpha_prev),
+            // delta = u^T K u (first step of a (re)start: beta = 0, alpha = gamma / delta).
+            if (sc->done) return;
+            double sb = 0.0, sh = 0.0, scs = 0.0;
+            for (int r = 0; r < P; ++r) {
+                sb += xa[r * 8 + 0];
+                sh += xa[r * 8 + 1];
+                scs += xa[r * 8 + 2];
+            }
+            const double gam = sum(3), rr = sum(4), gam_prev = sc->rho;
+            sc->S_b = sb;
+            sc->S_H = sh;
+            if (sc->spmv_split) sc->S_c = scs;
+            sc->rr = rr;
+            sc->rho_old = gam_prev;                   // rho = r^T u of the current residual, as
+            sc->rho = gam;                            // fin_pcg_update leaves it
+            if (!finite_d(rr) || !finite_d(gam)) {
+                sc->breakdown = 1;
+                sc->done = 1;
+                break;
+            }
+            if (rr <= sc->tol2 || sc->it >= sc->maxit) {
+                sc->done = 1;
+                break;
+            }
+            const double delta = sh + sb + sc->S_c;
+            const bool first = (sc->it_rs == 0);
+            const double beta = first ? 0.0 : gam / gam_prev;
+            const double den = first ? delta : delta - beta * gam / sc->alpha;
+            sc->pKp = den;
+            if (!(den > 0.0) || !finite_d(den)) {
+                sc->breakdown = 1;
+                sc->done = 1;
+                sc->alpha = 0.0;
+                break;
+            }
+            sc->alpha = gam / den;
+            sc->cg_beta = beta;
+            sc->cg_first = first ? 1 : 0;
+            sc->it += 1;
+            sc->it_rs += 1;
+            break;
+        }
         default:
             break;
     }

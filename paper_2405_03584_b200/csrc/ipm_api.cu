@@ -181,6 +181,7 @@ struct ipm_ctx {
     // peer-memory data plane (peer.h): device-side exchanges instead of Comm allgathers
     bool peer_on = false;
     bool a_split = false;        // PCG SpMV over this rank's rows of A only (peer plane, opt.a_row_split)
+    bool cg = false;             // Chronopoulos-Gear single-reduction PCG (sharded, opt.pcg_single_reduction)
     ipm::PeerArgs peer{};
     std::vector<void *> ipc_opened;
 };
@@ -513,6 +514,46 @@ ipm_status pcg_iteration_sharded(ipm_ctx *ctx, cudaStream_t st = nullptr, int us
     return IPM_OK;
 }
 
+// Chronopoulos-Gear single-reduction PCG (opt.pcg_single_reduction, sharded): the operator is
+// applied to u = M^-1 r; ONE scalar exchange per iteration (X_CG: S_b, S_H, S_c, r^T u, ||r||^2)
+// decides the stop and alpha, beta; p and s = K p follow by recurrence in k_cg_update.  The
+// standard loop needs two (X_PCG_ALPHA after the operator, X_PCG_UPDATE after the update).
+ipm_status pcg_iteration_cg(ipm_ctx *ctx, cudaStream_t st = nullptr, int use_cond = 0) {
+    const Prob &P = ctx->P;
+    const Vecs &V = ctx->V;
+    st = st ? st : ctx->st;
+    const double *uf = nullptr;
+    TRY(gather(ctx, V.pz, &uf, st, 1));
+    const bool par = P.m > 0;
+    if (par) {
+        cudaStream_t side = ctx->fork.side;
+        CK(cudaEventRecord(ctx->fork.ev_fork, st));
+        CK(cudaStreamWaitEvent(side, ctx->fork.ev_fork, 0));
+        const double *t = V.pt;
+        if (ctx->a_split) {
+            const PeerArgs &pa = ctx->peer;
+            double *tall = reinterpret_cast<double *>(pa.base[pa.rank] + pa.L.tall);
+            const int64_t m0 = peer_mrow0(pa, pa.rank), m1 = peer_mrow0(pa, pa.rank + 1);
+            launch_spmv_rows(P, uf, V.sig_c, tall, V.part[3], ctx->sc, m0, m1, side, side_block());
+            launch_peer_put_vec(pa, tall + m0, m1 - m0, pa.L.tall, m0, 1, ctx->sc, 1, side);
+            launch_peer_wait(pa, ctx->sc, -1, 0.0, 0.0, 0, 1, 0, 0, side, 1);
+            t = tall;
+        } else {
+            launch_spmv(P, uf, V.sig_c, V.pt, V.part[3], ctx->sc, 1, 1, side, kMaxGrid, side_block());
+        }
+        launch_pcg_spmvT(P, V, ctx->G, ctx->sc, t, side);
+        CK(cudaEventRecord(ctx->fork.ev_join, side));
+    }
+    launch_gemv(P, uf, V.pz, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 1, C_GEMV_PCG, st);
+    TRY(sym_exchange(ctx, st, 1));
+    if (par) CK(cudaStreamWaitEvent(st, ctx->fork.ev_join, 0));
+    TRY(xcombine(ctx, X_CG, 0.0, 0.0, 0, st, 1, ctx->handle, use_cond));
+    launch_cg_update(P, V, ctx->ncb, ctx->sc, V.dx, st);
+    ctx->launches += 3 + (P.m > 0 ? 2 : 0);
+    CKL();
+    return IPM_OK;
+}
+
 ipm_status build_graph(ipm_ctx *ctx) {
     if (ctx->graph_ready) return IPM_OK;
     CK(cudaGraphCreate(&ctx->graph, 0));
@@ -532,7 +573,8 @@ ipm_status build_graph(ipm_ctx *ctx) {
     const int unroll = ue ? std::max(1, std::min(8, atoi(ue))) : 1;
     if (ctx->sharded) {
         // peer data plane: the whole sharded iteration (puts, waits, combines) is device-side
-        TRY(pcg_iteration_sharded(ctx, ctx->cap, 1));
+        if (ctx->cg) TRY(pcg_iteration_cg(ctx, ctx->cap, 1));
+        else TRY(pcg_iteration_sharded(ctx, ctx->cap, 1));
     } else {
         for (int u = 0; u < unroll; ++u)
             launch_pcg_iteration(ctx->P, ctx->V, ctx->G, ctx->ncb, ctx->gemv_grid, ctx->sc, ctx->V.dx, ctx->handle,
@@ -589,6 +631,11 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) 
     const int per_it = (ctx->fused_p ? 2 : 3) + (P.m > 0 ? 2 : 0) +
                        (ctx->sharded && ctx->peer_on ? 6 + (ctx->sym_sharded ? 3 : 0) : 0);
     for (int round = 0;; ++round) {
+        if (ctx->cg) {                                      // gamma, ||r||^2, S_b of u = M^-1 r
+            launch_cg_prime(P, V, ctx->sc, ctx->st);
+            ctx->launches += 1;
+            CKL();
+        }
         if (ctx->fused_p && !small) {
             launch_pcg_p(P, V, ctx->sc, ctx->st);           // p = z after the (re)start; S_b
             ctx->launches += 1;
@@ -606,7 +653,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) 
             // host-driven batches; every rank sees the same combined `done`, so all ranks run
             // the same number of iterations and collectives
             for (;;) {
-                for (int b = 0; b < 16; ++b) TRY(pcg_iteration_sharded(ctx));
+                for (int b = 0; b < 16; ++b) TRY(ctx->cg ? pcg_iteration_cg(ctx) : pcg_iteration_sharded(ctx));
                 TRY(sync_scalars(ctx));
                 if (ctx->hsc->done) break;
             }
@@ -1050,6 +1097,7 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             const int64_t one = 1;
             CK(cudaMemcpyAsync(&ctx->sc->sharded, &one, sizeof one, cudaMemcpyHostToDevice, ctx->st));
             if ((s = setup_peer(ctx, ctx->ws + o.peer, ctx->ws + o.part)) != IPM_OK) return s;
+            ctx->cg = ctx->opt.pcg_single_reduction != 0 && ctx->opt.pcg_system == 0;
             if (p->comm_kind == 3 && !ctx->peer_on && ctx->comm->nranks > 1)
                 return fail(ctx, IPM_ERR_INVALID, "comm_kind 3 needs the peer data plane (2 <= nranks <= %d, "
                             "IPM_PEER not 0)", kPeerMax);

@@ -88,6 +88,10 @@ void launch_spmv_rows(const Prob &P, const double *v, const double *sigc, double
                       int64_t r0, int64_t r1, cudaStream_t st, int block);
 void launch_pcg_spmvT(const Prob &P, const Vecs &V, int G, Scalars *sc, const double *t, cudaStream_t st);
 void launch_pcg_update_only(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st);
+// Chronopoulos-Gear single-reduction PCG (sharded option, pcg.cu): priming after a (re)start and
+// the update (operator applied to u = V.pz; p = V.pp, s = K p = V.py by recurrence)
+void launch_cg_prime(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+void launch_cg_update(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x, cudaStream_t st);
 void configure_linalg_carveout();   // max-shared carveout for kernels co-running with the SYMV
 cudaError_t configure_linalg_attrs();   // >48 KB dynamic smem opt-ins (per device: called at every create)
 cudaError_t configure_pcg_attrs();

@@ -171,6 +171,130 @@ k_pcg_restart(int n, const double *__restrict__ r, double *__restrict__ z, const
     }
 }
 
+static int update_group(int ncb);
+
+// ---------------------------------------------- Chronopoulos-Gear PCG (sharded option)
+// One global reduction per iteration (the exchange X_CG, finalize.cuh) instead of two: the
+// operator is applied to u = M^-1 r (not to p), and p, s = K p follow by recurrence
+// (Chronopoulos & Gear 1989; the same iterates as Jacobi PCG in exact arithmetic).
+// Priming after a (re)start: this rank's gamma = r^T u, ||r||^2 and S_b = sum sig_b u^2.
+__global__ void __launch_bounds__(kBlock)
+k_cg_prime(int n, const double *__restrict__ r, const double *__restrict__ u, const double *__restrict__ sigb,
+           double *__restrict__ p1, double *__restrict__ p2, double *__restrict__ p3, Scalars *sc) {
+    __shared__ double red[kBlock / 32];
+    double g = 0.0, rr = 0.0, sb = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double ri = r[i], ui = u[i];
+        g = fma(ri, ui, g);
+        rr = fma(ri, ri, rr);
+        sb = fma(sigb[i] * ui, ui, sb);
+    }
+    const double a = block_sum(g, red), b = block_sum(rr, red), c = block_sum(sb, red);
+    if (threadIdx.x == 0) {
+        p1[blockIdx.x] = a;
+        p2[blockIdx.x] = b;
+        p3[blockIdx.x] = c;
+    }
+    if (last_block(&sc->counters[C_INIT_PCG])) {
+        const double ta = sum_partials(p1, gridDim.x, red), tb = sum_partials(p2, gridDim.x, red),
+                     tc = sum_partials(p3, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_INIT_PCG] = 0;
+            sc->loc[3] = ta;
+            sc->loc[4] = tb;
+            sc->loc[0] = tc;
+        }
+    }
+}
+
+// Update with w = K u assembled per row (tile partials + sigma_b u + A^T t):
+//   p = u + beta p,  s = w + beta s,  x += alpha p,  r -= alpha s,  u = M^-1 r
+// and the next exchange's partials gamma = r^T u, ||r||^2, S_b = sum sig_b u^2.
+template <int G>
+__global__ void __launch_bounds__(kBlock)
+k_cg_update(int n, int ncb, const double *__restrict__ ypart, const double *__restrict__ sigb,
+            double *__restrict__ u, const double *__restrict__ pAt, double *__restrict__ x, double *__restrict__ r,
+            double *__restrict__ p, double *__restrict__ s, const double *__restrict__ Minv, double *__restrict__ p1,
+            double *__restrict__ p2, double *__restrict__ p3, Scalars *sc) {
+    __shared__ double red[kBlock / 32];
+    if (sc->done) return;
+    const double alpha = sc->alpha, beta = sc->cg_beta;
+    const bool first = sc->cg_first != 0;
+    const int gl = threadIdx.x & (G - 1);
+    const int gpb = blockDim.x / G;
+    double ga = 0.0, rr = 0.0, sb = 0.0;
+    for (int gb_ = blockIdx.x * gpb + (int)(threadIdx.x & ~31u) / G; gb_ < n; gb_ += gridDim.x * gpb) {
+        const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
+        const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;
+        double ui = 0.0, sbi = 0.0, ati = 0.0, pi = 0.0, si = 0.0, xi = 0.0, ri = 0.0, mi = 0.0;
+        if (gl == 0) {
+            ui = u[i];
+            sbi = sigb[i];
+            if (pAt != nullptr) ati = pAt[i];
+            pi = p[i];
+            si = s[i];
+            xi = x[i];
+            ri = r[i];
+            mi = Minv[i];
+        }
+        double hs = 0.0;
+        for (int c = gl; c < ncb; c += G) hs += ypart[(int64_t)i * ncb + c];
+        hs = group_sum<G>(hs);
+        if (act && gl == 0) {
+            const double wi = fma(sbi, ui, hs + ati);             // (K u)_i, k_pcg_update's association
+            const double pn = first ? ui : fma(beta, pi, ui);
+            const double sn = first ? wi : fma(beta, si, wi);
+            p[i] = pn;
+            s[i] = sn;
+            x[i] = fma(alpha, pn, xi);
+            const double rn = fma(-alpha, sn, ri);
+            r[i] = rn;
+            const double un = mi * rn;
+            u[i] = un;
+            ga = fma(rn, un, ga);
+            rr = fma(rn, rn, rr);
+            sb = fma(sbi * un, un, sb);
+        }
+    }
+    const double a = block_sum(ga, red), b = block_sum(rr, red), c = block_sum(sb, red);
+    if (threadIdx.x == 0) {
+        p1[blockIdx.x] = a;
+        p2[blockIdx.x] = b;
+        p3[blockIdx.x] = c;
+    }
+    if (last_block(&sc->counters[C_UPD])) {
+        const double ta = sum_partials(p1, gridDim.x, red), tb = sum_partials(p2, gridDim.x, red),
+                     tc = sum_partials(p3, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[C_UPD] = 0;
+            sc->loc[3] = ta;
+            sc->loc[4] = tb;
+            sc->loc[0] = tc;
+        }
+    }
+}
+
+void launch_cg_prime(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
+    k_cg_prime<<<grid_for(P.n, kBlock), kBlock, 0, st>>>(P.n, V.pr, V.pz, V.sig_b, V.part[0], V.part[1], V.part[7],
+                                                         sc);
+}
+
+void launch_cg_update(const Prob &P, const Vecs &V, int ncb, Scalars *sc, double *x, cudaStream_t st) {
+    const int G = update_group(ncb);
+    const int ug = grid_for(P.n, kBlock / G);
+    const double *pAt = (P.m > 0) ? V.pAt : nullptr;
+#define IPM_CGU(GG)                                                                                              \
+    k_cg_update<GG><<<ug, kBlock, 0, st>>>(P.n, ncb, V.ypart, V.sig_b, V.pz, pAt, x, V.pr, V.pp, V.py, V.Minv,    \
+                                           V.part[5], V.part[6], V.part[7], sc)
+    switch (G) {
+        case 4: IPM_CGU(4); break;
+        case 8: IPM_CGU(8); break;
+        case 16: IPM_CGU(16); break;
+        default: IPM_CGU(32); break;
+    }
+#undef IPM_CGU
+}
+
 void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
     k_pcg_restart<<<grid_for(std::max(P.n, P.aug ? P.m : 0), kBlock), kBlock, 0, st>>>(
         P.n, V.pr, V.pz, V.Minv, V.part[0], V.part[1], sc, aug_args(P, V));
@@ -958,6 +1082,8 @@ void preload_pcg() {
     touch_kernel(k_pcg_update_fp<4, true, 1024>); touch_kernel(k_pcg_update_fp<8, true, 1024>);
     touch_kernel(k_pcg_small);
     touch_kernel(k_spmvT<4>); touch_kernel(k_spmvT<8>); touch_kernel(k_spmvT<16>); touch_kernel(k_spmvT<32>);
+    touch_kernel(k_cg_prime); touch_kernel(k_cg_update<4>); touch_kernel(k_cg_update<8>);
+    touch_kernel(k_cg_update<16>); touch_kernel(k_cg_update<32>);
 }
 
 }  // namespace ipm

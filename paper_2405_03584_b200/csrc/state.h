@@ -51,6 +51,9 @@ struct Scalars {
     unsigned long long peer_seq[2];      // per exchange channel (peer.h)
     unsigned int peer_ctr[2], peer_timeout;
     int64_t spmv_split;                  // 1: the PCG SpMV runs on this rank's A rows; S_c partial in loc[2]
+    // Chronopoulos-Gear single-reduction PCG (sharded option): beta of the update, first-step flag
+    double cg_beta;
+    int64_t cg_first;
     unsigned long long peer_diag[4];     // timeout: {expected seq, sender, its flag, stage + 1000}
     unsigned int counters[kNumCounters];
     // --- live launch timing of the PCG operator kernel (bench.py roofline) ---------------
@@ -67,7 +70,8 @@ struct Scalars {
 };
 
 // Combine stages of k_xcombine (shard.cu).
-enum XStage { X_PCG_INIT = 0, X_PCG_ALPHA, X_PCG_UPDATE, X_PCG_RESTART, X_RES2, X_SUMLS, X_RESID, X_RECOVER, X_MUAFF };
+enum XStage { X_PCG_INIT = 0, X_PCG_ALPHA, X_PCG_UPDATE, X_PCG_RESTART, X_RES2, X_SUMLS, X_RESID, X_RECOVER, X_MUAFF,
+              X_CG };
 
 enum Counter {
     C_GEMV = 0, C_GEMV_PCG, C_SPMV, C_SPMV_PCG, C_P, C_UPD, C_INIT_PCG, C_TRUE_RES, C_INIT_M, C_INIT_N,

@@ -180,3 +180,34 @@ def test_a_row_split_spmv(P):
     assert abs(stats[0]["ipm_iters"] - stats_r[0]["ipm_iters"]) <= 1
     ref = solve(Problem.from_data(q))
     assert np.max(np.abs(x - ref.x)) <= 1e-6 * max(1.0, np.max(np.abs(ref.x)))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_single_reduction_pcg(P):
+    """Chronopoulos-Gear single-reduction PCG (opt.pcg_single_reduction, SURVEY NEXT-3's sharded
+    variant): one scalar exchange per iteration.  Its k-step iterates equal the textbook PCG's
+    (oracle.pcg) to rounding, and the IPM solve matches the oracle."""
+    from oracle.pcg import pcg as oracle_pcg
+    from paper_2405_03584_b200.dist import partition
+    q = planted_qp(1200, 400, density=0.02, rank=32, seed=70 + P, rows="vmat", var="box")
+    grp, qps = _sharded(q, P, pcg_single_reduction=1)
+    rng = np.random.default_rng(3)
+    sb, sc, b = rng.uniform(0.0, 3.0, q.n), 10.0 ** rng.uniform(-2, 2, q.m), rng.normal(size=q.n)
+    parts = partition(q.n, P)
+    A = q.A_scipy()
+    K_apply = lambda v: q.H @ v + sb * v + A.T @ (sc * (A @ v))   # noqa: E731
+    Minv = 1.0 / (np.diag(q.H) + sb + (A.multiply(A)).T @ sc)
+    for k in (1, 3, 6):
+        outs = grp.run([lambda qq=qq, r=r: qq.pcg_iterate(sb[parts[r][0]:parts[r][1]], sc,
+                                                          b[parts[r][0]:parts[r][1]], k)
+                        for r, qq in enumerate(qps)])
+        ref = oracle_pcg(K_apply, Minv, b, maxit=k)
+        for key, refv in (("x", ref.x), ("r", ref.r), ("p", ref.p)):
+            g = np.concatenate([o[key].cpu().numpy() for o in outs])
+            assert np.max(np.abs(g - refv)) <= 1e-10 * np.max(np.abs(refv)), (P, k, key)
+        assert abs(outs[0]["alpha"] - ref.alpha) <= 1e-10 * abs(ref.alpha)
+    st, x, stats = _solve_all(grp, qps)
+    assert st == ["ok"] * P and len({s["obj"] for s in stats}) == 1
+    ref = solve(Problem.from_data(q))
+    assert np.max(np.abs(x - ref.x)) <= 1e-6 * max(1.0, np.max(np.abs(ref.x)))
+    assert abs(stats[0]["ipm_iters"] - ref.iters) <= 2
