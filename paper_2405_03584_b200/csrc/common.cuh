@@ -41,6 +41,23 @@ __device__ __forceinline__ double group_sum(double v) {
     return v;
 }
 
+// Lane gl's part of a GEMV tile-partial row sum: row[gl] + row[gl + G] + ... added in that
+// order, with four loads in flight per trip (bitwise the plain strided loop).
+template <int G>
+__device__ __forceinline__ double row_part_sum(const double *__restrict__ row, int gl, int ncb) {
+    double s = 0.0;
+    int c = gl;
+    for (; c + 3 * G < ncb; c += 4 * G) {
+        const double a0 = row[c], a1 = row[c + G], a2 = row[c + 2 * G], a3 = row[c + 3 * G];
+        s += a0;
+        s += a1;
+        s += a2;
+        s += a3;
+    }
+    for (; c < ncb; c += G) s += row[c];
+    return s;
+}
+
 // Block-wide sum; result valid in ALL threads.  `sh` needs blockDim/32 doubles.
 __device__ __forceinline__ double block_sum(double v, double *sh) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;

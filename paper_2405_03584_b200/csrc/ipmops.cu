@@ -225,7 +225,7 @@ k_resid_n(int n, int ncb, const double *__restrict__ ypart, const int64_t *__res
         const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
         const int j = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double hs = 0.0, at = 0.0;
-        for (int c = gl; c < ncb; c += G) hs += ypart[(int64_t)j * ncb + c];
+        hs += row_part_sum<G>(ypart + (int64_t)j * ncb, gl, ncb);
         if (lamd != nullptr) {
             const int64_t e = ATrp[j + 1];
             for (int64_t k = ATrp[j] + gl; k < e; k += G) at = fma(__ldg(ATval + k), __ldg(lamd + __ldg(ATcol + k)), at);

@@ -1046,7 +1046,7 @@ k_apply_reduce(int n, int ncb, const double *__restrict__ ypart, const double *_
         const bool act = gb_ + (int)(threadIdx.x & 31u) / G < n;
         const int i = act ? gb_ + (int)(threadIdx.x & 31u) / G : n - 1;   // idle lanes re-read row n-1, write nothing
         double s = 0.0;
-        for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
+        s += row_part_sum<G>(ypart + (int64_t)i * ncb, gl, ncb);
         if (MODE != 2 && t != nullptr) {
             const int64_t e = ATrp[i + 1];
             for (int64_t k = ATrp[i] + gl; k < e; k += G) s = fma(__ldg(ATval + k), __ldg(t + __ldg(ATcol + k)), s);

@@ -238,7 +238,7 @@ k_cg_update(int n, int ncb, const double *__restrict__ ypart, const double *__re
             mi = Minv[i];
         }
         double hs = 0.0;
-        for (int c = gl; c < ncb; c += G) hs += ypart[(int64_t)i * ncb + c];
+        hs += row_part_sum<G>(ypart + (int64_t)i * ncb, gl, ncb);
         hs = group_sum<G>(hs);
         if (act && gl == 0) {
             const double wi = fma(sbi, ui, hs + ati);             // (K u)_i, k_pcg_update's association
@@ -402,7 +402,7 @@ k_pcg_update(int n, int ncb, const double *__restrict__ ypart, const double *__r
             if (pAt != nullptr) ati = pAt[i];
         }
         double s = 0.0;
-        for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
+        s += row_part_sum<G>(ypart + (int64_t)i * ncb, gl, ncb);
         s = group_sum<G>(s);
         if (act && gl == 0) {
             const double yi = fma(sbi, pi, s + ati);   // (H p)_i + sigma_b p_i + (A^T t)_i
@@ -505,7 +505,7 @@ k_pcg_update_fp(int n, int ncb, const double *__restrict__ ypart, const double *
             if (pAt != nullptr) ati = pAt[i];
         }
         double s = 0.0;
-        for (int c = gl; c < ncb; c += G) s += ypart[(int64_t)i * ncb + c];
+        s += row_part_sum<G>(ypart + (int64_t)i * ncb, gl, ncb);
         s = group_sum<G>(s);
         if (act && gl == 0) {
             const double yi = fma(sbi, pi, s + ati);
