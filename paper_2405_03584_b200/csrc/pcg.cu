@@ -754,7 +754,8 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
         sb[i] = sigb[i];
     }
     if (h_in_smem)
-        for (int64_t e = tid; e < (int64_t)n * n; e += blockDim.x) sH[e] = H[(e / n) * ldh + e % n];
+        for (int i = warp; i < n; i += nw)         // a warp per row: no 64-bit index division
+            for (int j = lane; j < n; j += 32) sH[(int64_t)i * n + j] = H[(int64_t)i * ldh + j];
     // A, A^T (CSR, int32 offsets) and sigma_c staged in shared memory too when they fit: every
     // phase then runs at shared-memory latency (same loops, same association: bitwise unchanged)
     if (a_in_smem) {
@@ -781,11 +782,187 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
 }
 
 
+
+// ------------------------------------------------------------- tiny problems: one WARP
+// For n <= 64 (C1: n = 50, m = 20) the PCG loop runs in ONE warp with every operand in shared
+// memory: lane l owns rows l and l + 32 of every x-space vector, rows l, l + 32, ... of A; the
+// phases are separated by __syncwarp only and every reduction is a 5-step xor-shuffle tree —
+// no block barriers (k_pcg_small's 6 per iteration).  Same recurrence and stopping rule.
+constexpr int kWarpMaxN = 64;
+
+__global__ void __launch_bounds__(32)
+k_pcg_warp(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_t *__restrict__ Arp,
+           const int *__restrict__ Acol, const double *__restrict__ Aval, const int64_t *__restrict__ ATrp,
+           const int *__restrict__ ATcol, const double *__restrict__ ATval, const double *__restrict__ sigb,
+           const double *__restrict__ sigc, const double *__restrict__ Minv, double *x, double *r, double *z,
+           double *p, double *t, double *y, Scalars *sc, int64_t nnz) {
+    extern __shared__ __align__(16) double sm[];
+    if (sc->done) return;
+    const int l = threadIdx.x;
+    const int hs = n | 1;                          // odd row stride: conflict-free column access
+    double *sp = sm, *st = sm + kWarpMaxN, *sH = st + m, *scg = sH + (int64_t)n * hs, *aval = scg + m,
+           *atval = aval + nnz;
+    int *arp = reinterpret_cast<int *>(atval + nnz), *acol = arp + (m + 1), *atrp = acol + nnz, *atcol = atrp + (n + 1);
+    for (int i = 0; i < n; ++i)                    // row by row: no 64-bit index division
+        for (int j = l; j < n; j += 32) sH[(int64_t)i * hs + j] = H[(int64_t)i * ldh + j];
+    for (int i = l; i < m; i += 32) scg[i] = sigc[i];
+    for (int i = l; i <= m; i += 32) arp[i] = (int)Arp[i];
+    for (int i = l; i <= n; i += 32) atrp[i] = (int)ATrp[i];
+    for (int64_t k = l; k < nnz; k += 32) {
+        aval[k] = Aval[k];
+        acol[k] = Acol[k];
+        atval[k] = ATval[k];
+        atcol[k] = ATcol[k];
+    }
+    // this lane's rows (registers): i0 = l, i1 = l + 32
+    const int i0 = l, i1 = l + 32;
+    const bool h0 = i0 < n, h1 = i1 < n;
+    double p0 = h0 ? p[i0] : 0.0, p1 = h1 ? p[i1] : 0.0, r0 = h0 ? r[i0] : 0.0, r1 = h1 ? r[i1] : 0.0;
+    double z0 = h0 ? z[i0] : 0.0, z1 = h1 ? z[i1] : 0.0, x0 = h0 ? x[i0] : 0.0, x1 = h1 ? x[i1] : 0.0;
+    const double m0 = h0 ? Minv[i0] : 0.0, m1 = h1 ? Minv[i1] : 0.0, b0 = h0 ? sigb[i0] : 0.0,
+                 b1 = h1 ? sigb[i1] : 0.0;
+    double y0 = 0.0, y1 = 0.0;
+    double rho = sc->rho, rho_old = sc->rho_old, rr = sc->rr, pkp = 0.0, alpha_last = 0.0;
+    int64_t it = sc->it, it_rs = sc->it_rs;
+    const double tol2 = sc->tol2;
+    const int64_t maxit = sc->maxit;
+    int breakdown = 0;
+    // (H p)_i + (A^T t)_i with four independent FMA chains (fp64 FMA latency, not throughput,
+    // bounds a lane's row), combined in a fixed order
+    auto row_dot = [&](int i) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+        const double *__restrict__ h = sH + (int64_t)i * hs;
+        int j = 0;
+        for (; j + 7 < n; j += 8) {                // 8 chains: 16 shared loads in flight per lane
+            a0 = fma(h[j], sp[j], a0);
+            a1 = fma(h[j + 1], sp[j + 1], a1);
+            a2 = fma(h[j + 2], sp[j + 2], a2);
+            a3 = fma(h[j + 3], sp[j + 3], a3);
+            e0 = fma(h[j + 4], sp[j + 4], e0);
+            e1 = fma(h[j + 5], sp[j + 5], e1);
+            e2 = fma(h[j + 6], sp[j + 6], e2);
+            e3 = fma(h[j + 7], sp[j + 7], e3);
+        }
+        for (; j < n; ++j) a0 = fma(h[j], sp[j], a0);
+        a0 += e0;
+        a1 += e1;
+        a2 += e2;
+        a3 += e3;
+        int k = atrp[i];
+        const int ke = atrp[i + 1];
+        for (; k + 1 < ke; k += 2) {
+            a1 = fma(atval[k], st[atcol[k]], a1);
+            a3 = fma(atval[k + 1], st[atcol[k + 1]], a3);
+        }
+        if (k < ke) a2 = fma(atval[k], st[atcol[k]], a2);
+        return (a0 + a1) + (a2 + a3);
+    };
+    __syncwarp();
+    for (;;) {
+        const bool first = (it_rs == 0);
+        const double beta = first ? 0.0 : rho / rho_old;
+        p0 = first ? z0 : fma(beta, p0, z0);
+        p1 = first ? z1 : fma(beta, p1, z1);
+        if (h0) sp[i0] = p0;
+        if (h1) sp[i1] = p1;
+        __syncwarp();
+        for (int i = l; i < m; i += 32) {          // t = sig_c o (A p), two chains per row
+            double a = 0.0, c = 0.0;
+            int k = arp[i];
+            const int ke = arp[i + 1];
+            for (; k + 1 < ke; k += 2) {
+                a = fma(aval[k], sp[acol[k]], a);
+                c = fma(aval[k + 1], sp[acol[k + 1]], c);
+            }
+            if (k < ke) a = fma(aval[k], sp[acol[k]], a);
+            st[i] = scg[i] * (a + c);
+        }
+        __syncwarp();
+        y0 = h0 ? fma(b0, p0, row_dot(i0)) : 0.0;
+        y1 = h1 ? fma(b1, p1, row_dot(i1)) : 0.0;
+        // p^T K p = p^T y (y = H p + sig_b p + A^T t, as k_pcg_small), xor-tree over the lanes
+        double d = fma(p0, y0, p1 * y1);
+        d = warp_sum(d);
+        pkp = d;
+        if (!(pkp > 0.0) || !finite_d(pkp)) {
+            breakdown = 1;
+            break;
+        }
+        const double alpha = rho / pkp;
+        alpha_last = alpha;
+        x0 = fma(alpha, p0, x0);
+        x1 = fma(alpha, p1, x1);
+        r0 = fma(-alpha, y0, r0);
+        r1 = fma(-alpha, y1, r1);
+        z0 = m0 * r0;
+        z1 = m1 * r1;
+        double rz = fma(r1, z1, r0 * z0), r2 = fma(r1, r1, r0 * r0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            rz += __shfl_xor_sync(0xffffffffu, rz, o);
+            r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        }
+        rho_old = rho;
+        rho = rz;
+        rr = r2;
+        ++it;
+        ++it_rs;
+        if (!finite_d(rr) || !finite_d(rho)) {
+            breakdown = 1;
+            break;
+        }
+        if (rr <= tol2 || it >= maxit) break;
+        __syncwarp();                              // st / sp reads done before the next overwrite
+    }
+    if (h0) {
+        p[i0] = p0; r[i0] = r0; z[i0] = z0; x[i0] = x0; y[i0] = y0;
+    }
+    if (h1) {
+        p[i1] = p1; r[i1] = r1; z[i1] = z1; x[i1] = x1; y[i1] = y1;
+    }
+    __syncwarp();
+    for (int i = l; i < m; i += 32) t[i] = st[i];
+    if (l == 0) {
+        sc->rho = rho;
+        sc->rho_old = rho_old;
+        sc->rr = rr;
+        sc->pKp = pkp;
+        sc->alpha = alpha_last;
+        sc->it = it;
+        sc->it_rs = it_rs;
+        sc->done = 1;
+        if (breakdown) sc->breakdown = 1;
+    }
+}
+
+static size_t warp_smem_bytes(const Prob &P) {
+    const size_t n = P.n, m = P.m, nnz = P.nnz;
+    return 8 * (kWarpMaxN + m + n * (n | 1) + m + 2 * nnz) + 4 * (m + 1 + n + 1 + 2 * nnz);
+}
+
+static int pcg_warp_enabled() {
+    static int e = -1;
+    if (e < 0) {
+        const char *v = getenv("IPM_PCG_WARP");      // experiment switch: 0 = always k_pcg_small
+        e = v ? atoi(v) : 1;
+    }
+    return e;
+}
+
 cudaError_t configure_pcg_attrs() {
-    return cudaFuncSetAttribute(k_pcg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
+    cudaError_t e = cudaFuncSetAttribute(k_pcg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
+    const cudaError_t e2 = cudaFuncSetAttribute(k_pcg_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)kSmallSmemMax);
+    return e != cudaSuccess ? e : e2;
 }
 
 void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cudaStream_t st) {
+    if (pcg_warp_enabled() && P.n <= kWarpMaxN && warp_smem_bytes(P) <= kSmallSmemMax) {
+        k_pcg_warp<<<1, 32, warp_smem_bytes(P), st>>>(P.n, P.m, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol,
+                                                       P.ATval, V.sig_b, V.sig_c, V.Minv, x, V.pr, V.pz, V.pp, V.pt,
+                                                       V.py, sc, P.nnz);
+        return;
+    }
     size_t bytes = 7 * (size_t)P.n * 8;
     const int t_in = (bytes + (size_t)P.m * 8 <= kSmallSmemMax) ? 1 : 0;
     if (t_in) bytes += (size_t)P.m * 8;
@@ -1081,6 +1258,7 @@ void preload_pcg() {
     touch_kernel(k_pcg_update_fp<4, true, kBlock>); touch_kernel(k_pcg_update_fp<8, true, kBlock>);
     touch_kernel(k_pcg_update_fp<4, true, 1024>); touch_kernel(k_pcg_update_fp<8, true, 1024>);
     touch_kernel(k_pcg_small);
+    touch_kernel(k_pcg_warp);
     touch_kernel(k_spmvT<4>); touch_kernel(k_spmvT<8>); touch_kernel(k_spmvT<16>); touch_kernel(k_spmvT<32>);
     touch_kernel(k_cg_prime); touch_kernel(k_cg_update<4>); touch_kernel(k_cg_update<8>);
     touch_kernel(k_cg_update<16>); touch_kernel(k_cg_update<32>);
