@@ -35,6 +35,7 @@ ap.add_argument("--out", default=None)
 ap.add_argument("--ckpt", default=None)
 ap.add_argument("--resume", default=None)
 ap.add_argument("--max-minutes", type=float, default=1e9)
+ap.add_argument("--stop-after", type=int, default=None, help="stop before QP k (resume testing)")
 a = ap.parse_args()
 t_wall = time.time()
 kw = {}
@@ -64,7 +65,7 @@ def emit(rec):
 
 
 for k in range(k0, a.K):
-    if time.time() - t_wall > a.max_minutes * 60:
+    if time.time() - t_wall > a.max_minutes * 60 or (a.stop_after is not None and k >= a.stop_after):
         emit({"stop": "time_limit", "next_qp": k})
         break
     if k > 0:
