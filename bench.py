@@ -266,10 +266,13 @@ def run_ours(args):
     from paper_2405_03584_b200 import QP
 
     ws, rank, local = _dist()
+    if args.same_gpu:       # testing the N > 1 paths on one GPU: every rank on cuda:0, gloo bootstrap
+        local = 0
     if ws > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if args.same_gpu else "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    rdev = torch.device("cpu") if args.same_gpu else dev    # device of the cross-rank reductions
     # C5 at N > 1 (or --shard): ONE QP row-sharded over the ranks (NCCL allgathers inside libipm,
     # SURVEY §8(e)), each rank building only its row block of H on its device; otherwise every
     # rank solves its own QP (seed + rank): replicas, no collective on the data path.
@@ -288,6 +291,12 @@ def run_ours(args):
         rows = partition(n, ws)[rank]
 
         def shard():
+            if args.same_gpu and ws > 1:
+                # processes sharing one GPU cannot form an NCCL communicator: bootstrap the peer
+                # data plane over the gloo group instead (comm_kind 3, CUDA IPC between processes)
+                from paper_2405_03584_b200.dist import host_shard, torch_allgather_bytes
+                uid_holder["s"] = host_shard(rank, ws, torch_allgather_bytes())
+                return uid_holder["s"]
             uid = (nccl_unique_id() if ws == 1
                    else broadcast_unique_id(nccl_unique_id, rank, dist.broadcast_object_list))
             uid_holder["s"] = nccl_shard(rank, ws, uid)
@@ -335,8 +344,8 @@ def run_ours(args):
     kt_ms, kt_n = kt1[0] - kt0[0], kt1[1] - kt0[1]
     t_s = e0.elapsed_time(e1) / 1e3
     pcg_local = sum(s["pcg_iters_total"] for s in stats)
-    tt = torch.tensor([t_s], dtype=torch.float64, device=dev)
-    pc = torch.tensor([float(pcg_local)], dtype=torch.float64, device=dev)
+    tt = torch.tensor([t_s], dtype=torch.float64, device=rdev)
+    pc = torch.tensor([float(pcg_local)], dtype=torch.float64, device=rdev)
     if ws > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         if not sharded:
@@ -386,8 +395,8 @@ def run_ours(args):
     e2e_t = time.perf_counter() - a0
     qp2.close()
     del qp2
-    te = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-    pe = torch.tensor([float(e2e_pcg)], dtype=torch.float64, device=dev)
+    te = torch.tensor([e2e_t], dtype=torch.float64, device=rdev)
+    pe = torch.tensor([float(e2e_pcg)], dtype=torch.float64, device=rdev)
     if ws > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         if not sharded:
@@ -465,6 +474,8 @@ def main():
     ap.add_argument("--shard", "--force-shard", dest="force_shard", action="store_true",
                     help="row-shard ONE QP over the N ranks (default only for C5 at N > 1) — also at N = 1 (NCCL path)")
     ap.add_argument("--no-extra", action="store_true", help="skip the C1/C2/C3 QP time-to-solution context")
+    ap.add_argument("--same-gpu", action="store_true",
+                    help="testing only: every rank on cuda:0 (gloo bootstrap, CUDA IPC data plane)")
     ap.add_argument("--host-loop", action="store_true",
                     help="profiling only: drive the PCG from the host (batches of 16) instead of the conditional-"
                          "WHILE graph, whose kernel nodes ncu cannot profile one by one")

@@ -54,3 +54,27 @@ def test_bench_driver_flags_c3_within_budget():
 def test_bench_c1_single_cta_path():
     d, _ = _run("--workload", "C1", "--steps", "3", "--warmup", "3", "--no-extra", "--no-cpu-baseline")
     assert d["value"] > 0 and d["roofline"]["launches_timed"] == 0 and d["cpu_baseline"] is None
+
+
+def test_bench_two_ranks_sharded_same_gpu():
+    """The N > 1 branch of bench.py (torchrun, barriers, max over ranks, the row-sharded QP with
+    the peer data plane, e2e) on one GPU: two processes share cuda:0 (--same-gpu: gloo bootstrap,
+    CUDA IPC exchanges), C3 forced sharded."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, IPM_PEER_TIMEOUT_S="60")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--same-gpu", "--workload", "C3", "--shard", "--steps", "1", "--warmup", "1",
+                        "--no-extra", "--no-cpu-baseline"], capture_output=True, text=True, timeout=1200, cwd=ROOT,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("row-sharded")
+    assert d["pcg_iters_per_step"] == [67]          # the same first IPM iteration as one GPU (C3 seed 0)
