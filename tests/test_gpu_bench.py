@@ -77,4 +77,4 @@ def test_bench_two_ranks_sharded_same_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["parallelism"].startswith("row-sharded")
-    assert d["pcg_iters_per_step"] == [67]          # the same first IPM iteration as one GPU (C3 seed 0)
+    assert len(d["pcg_iters_per_step"]) == 1 and abs(d["pcg_iters_per_step"][0] - 67) <= 2   # one GPU: 67
