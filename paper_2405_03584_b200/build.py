@@ -36,7 +36,9 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
              "pf1": ["-DIPM_SYM_PF=1"], "pf2": ["-DIPM_SYM_PF=2"], "pf3": ["-DIPM_SYM_PF=3"],
              "pf4": ["-DIPM_SYM_PF=4"], "pf6": ["-DIPM_SYM_PF=6"], "pf3nc": ["-DIPM_SYM_PF=3", "-DIPM_SYM_NOCOMPUTE"],
              "lds4": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=4"], "lds2": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=2"],
-             "lds6": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=6"], "lds4nc": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_NOCOMPUTE"]}.get(variant, [])
+             "lds6": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=6"], "lds4nc": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_NOCOMPUTE"],
+             "ncldg2": ["-DIPM_SYM_NOCOMPUTE", "-DIPM_SYM_LDGW=2"], "ncldg3": ["-DIPM_SYM_NOCOMPUTE", "-DIPM_SYM_LDGW=3"],
+             "ldg2": ["-DIPM_SYM_LDGW=2"]}.get(variant, [])
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers += [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
     objdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))

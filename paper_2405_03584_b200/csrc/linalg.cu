@@ -349,7 +349,18 @@ constexpr int kSymLoaders = IPM_SYM_LOADERS;
 #else
 constexpr int kSymLoaders = 1;
 #endif
-constexpr int kSymThreads = 32 * (kSymConsumers + kSymLoaders);
+#ifndef IPM_SYM_LDGW
+#define IPM_SYM_LDGW 0
+#endif
+// experiment (build variant "ncldg"): extra warps that stream other rows of H with LDG.128 next to
+// the TMA ring, to see whether the LSU path adds bandwidth on top of the TMA unit's
+constexpr int kSymLdgW = IPM_SYM_LDGW;
+constexpr int kSymThreads = 32 * (kSymConsumers + kSymLoaders + kSymLdgW);
+#if IPM_SYM_LDGW > 0
+__device__ const double *g_ldg_H;
+__device__ long long g_ldg_ldh, g_ldg_rows, g_ldg_n;
+__device__ double g_ldg_sink;
+#endif
 constexpr int kSymRW = kSymSR / kSymConsumers;    // strip rows reduced by each consumer warp
 constexpr int kSymStageDoubles = kSymSR * kSymB + kSymB + kSymSR;
 constexpr size_t kSymSmem = (size_t)kSymStages * kSymStageDoubles * 8 + 2 * kSymStages * 8;
@@ -495,6 +506,25 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
         }
     } else if (false) {
 #else
+#if IPM_SYM_LDGW > 0
+    if (warp > kSymConsumers) {
+        const int lw = warp - kSymConsumers - 1;
+        const long long r0 = (long long)blockIdx.x * g_ldg_rows, r1 = r0 + g_ldg_rows;
+        double acc = 0.0;
+        const int n2 = (int)(g_ldg_n / 2);
+        for (long long row = r0 + lw; row < r1; row += kSymLdgW) {
+            const double2 *rp = reinterpret_cast<const double2 *>(g_ldg_H + row * g_ldg_ldh);
+            for (int k = lane; k < n2; k += 32 * 8) {
+                double2 v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = (k + 32 * q < n2) ? __ldcs(rp + k + 32 * q) : make_double2(0, 0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc += v[q].x * v[q].y;
+            }
+        }
+        if (acc == 1.2345e300) g_ldg_sink = acc;
+    } else
+#endif
     if (warp == kSymConsumers) {
 #endif
         if (lane == 0) {
@@ -672,6 +702,18 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
 
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
                       int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot) {
+#if IPM_SYM_LDGW > 0
+    {
+        const char *e = getenv("IPM_SYM_LDGROWS");
+        const long long rows = e ? atoll(e) : 34, ldh = P.ldh, n = P.ncols;
+        const double *h = P.H;
+        cudaMemcpyToSymbolAsync(g_ldg_H, &h, sizeof h, 0, cudaMemcpyHostToDevice, st);
+        cudaMemcpyToSymbolAsync(g_ldg_ldh, &ldh, sizeof ldh, 0, cudaMemcpyHostToDevice, st);
+        cudaMemcpyToSymbolAsync(g_ldg_rows, &rows, sizeof rows, 0, cudaMemcpyHostToDevice, st);
+        cudaMemcpyToSymbolAsync(g_ldg_n, &n, sizeof n, 0, cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);       // host stack values
+    }
+#endif
 #ifdef IPM_SYM_LDGSTS
     CUtensorMap raw;
     SymRaw *sr = reinterpret_cast<SymRaw *>(&raw);
