@@ -50,15 +50,19 @@ def test_options_default_and_abi(lib):
 def test_struct_sizes_match_c(lib, tmp_path):
     """Compile a tiny C program against include/ipm.h and compare sizeof/offsetof with ctypes."""
     src = tmp_path / "sz.c"
-    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ipm.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu\\n",'
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ipm.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n",'
                    'sizeof(ipm_options), sizeof(ipm_problem), sizeof(ipm_stats), sizeof(ipm_trace_rec),'
-                   'offsetof(ipm_options, warm_shift), offsetof(ipm_problem, comm_handle_host));return 0;}\n')
+                   'offsetof(ipm_options, warm_shift), offsetof(ipm_problem, comm_handle_host),'
+                   'offsetof(ipm_options, a_row_split), offsetof(ipm_options, kernel_timer),'
+                   'sizeof(ipm_host_comm), offsetof(ipm_host_comm, user));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     assert vals == [C.sizeof(lib.ipm_options), C.sizeof(lib.ipm_problem), C.sizeof(lib.ipm_stats),
                     C.sizeof(lib.ipm_trace_rec), lib.ipm_options.warm_shift.offset,
-                    lib.ipm_problem.comm_handle_host.offset]
+                    lib.ipm_problem.comm_handle_host.offset, lib.ipm_options.a_row_split.offset,
+                    lib.ipm_options.kernel_timer.offset, C.sizeof(lib.ipm_host_comm), lib.ipm_host_comm.user.offset]
 
 
 def test_workspace_size_host_only(lib):
