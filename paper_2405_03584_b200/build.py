@@ -38,7 +38,9 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
              "lds4": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=4"], "lds2": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=2"],
              "lds6": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_LOADERS=6"], "lds4nc": ["-DIPM_SYM_LDGSTS", "-DIPM_SYM_NOCOMPUTE"],
              "ncldg2": ["-DIPM_SYM_NOCOMPUTE", "-DIPM_SYM_LDGW=2"], "ncldg3": ["-DIPM_SYM_NOCOMPUTE", "-DIPM_SYM_LDGW=3"],
-             "ldg2": ["-DIPM_SYM_LDGW=2"]}.get(variant, [])
+             "ldg2": ["-DIPM_SYM_LDGW=2"],
+             "hyb10": ["-DIPM_SYM_LDGW=2", "-DIPM_SYM_LDG_EVERY=10"], "hyb7": ["-DIPM_SYM_LDGW=2", "-DIPM_SYM_LDG_EVERY=7"],
+             "hyb14": ["-DIPM_SYM_LDGW=2", "-DIPM_SYM_LDG_EVERY=14"], "hyb10w3": ["-DIPM_SYM_LDGW=3", "-DIPM_SYM_LDG_EVERY=10"]}.get(variant, [])
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers += [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
     objdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))

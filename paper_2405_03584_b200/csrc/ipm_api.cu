@@ -1251,6 +1251,8 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
             P.sym_tiles = dt;
             P.sym_ranges = dr;
             P.sym_z = reinterpret_cast<double *>(ctx->ws + o.symz);
+            P.sym_ntma = symp.ntma;
+            P.sym_ntiles = (int)symp.tiles.size();
             P.sym_ycarry = symp.nbg;
             P.sym_ldz = symp.ldz;
             P.sym_zcarry = symp.ldz - symp.zcarry_n;

@@ -49,11 +49,17 @@ struct SymRange {
     int pad[3];
 };
 struct SymPlan {
-    std::vector<SymTile> tiles;
+    std::vector<SymTile> tiles;     // [0, ntma): streamed through the TMA ring (ranges); [ntma, size):
+                                    // whole tiles for the LDG warps (hybrid build), CTA b takes
+                                    // ntma + b, ntma + b + grid, ...
     std::vector<SymRange> ranges;
     std::vector<int> zcol;          // global column of each zpart row
-    int nbg = 0, ycarry_n = 0, zcarry_n = 0, ldy = 0, ldz = 0, zrows = 0;
+    int nbg = 0, ycarry_n = 0, zcarry_n = 0, ldy = 0, ldz = 0, zrows = 0, ntma = 0;
 };
+#ifndef IPM_SYM_LDG_EVERY
+#define IPM_SYM_LDG_EVERY 0
+#endif
+constexpr int kSymLdgEvery = IPM_SYM_LDG_EVERY;   // hybrid SYMV: every k-th off-diagonal tile to LDG warps
 void sym_plan_build(int ncols, int nranks, int rank, int grid, SymPlan &plan);
 
 // linalg.cu

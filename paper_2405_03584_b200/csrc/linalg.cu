@@ -436,7 +436,8 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
             const SymRange *__restrict__ ranges, const double *__restrict__ p, int64_t row_begin,
             const double *__restrict__ pdot, double *__restrict__ ypart, int ldy, int ycarry,
             double *__restrict__ zpart, int ldz, int zcarry, double *__restrict__ dpart, Scalars *sc, int cid,
-            int keep, const double *__restrict__ sigb_dot, int timed) {
+            int keep, const double *__restrict__ sigb_dot, int timed, const double *__restrict__ Hraw,
+            int64_t ldh_raw, int ntma, int ntiles) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[kSymThreads / 32];
     __shared__ double colbuf[kSymB];                  // row-half-1 column sums of the current tile
@@ -506,7 +507,79 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
         }
     } else if (false) {
 #else
-#if IPM_SYM_LDGW > 0
+#if IPM_SYM_LDGW > 0 && IPM_SYM_LDG_EVERY > 0
+    if (warp > kSymConsumers) {
+        // hybrid: whole off-diagonal tiles straight from global memory (LDG.128, evict-first)
+        // next to the TMA ring; lane owns columns c = 2 lane + 64 q + {0, 1} (q < 4), two rows in
+        // flight; the row parts are reduced with a butterfly that leaves row r's sum in lanes
+        // 16 r .. 16 r + 15, the column parts accumulate per lane over all 256 rows
+        const int lw = warp - kSymConsumers - 1;
+        for (int t = ntma + blockIdx.x + lw * (int)gridDim.x; t < ntiles; t += (int)gridDim.x * kSymLdgW) {
+            const SymTile T = tiles[t];
+            const double *Hb = Hraw;
+            double2 pj[4], ca[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c = 2 * lane + 64 * q;
+                pj[q] = (c < T.cols) ? *reinterpret_cast<const double2 *>(p + T.c0 + c) : make_double2(0.0, 0.0);
+                ca[q] = make_double2(0.0, 0.0);
+            }
+            for (int r = 0; r < T.rows; r += 2) {
+                const bool two = r + 1 < T.rows;
+                const double2 *h0 = reinterpret_cast<const double2 *>(Hb + (int64_t)(T.r0 + r) * ldh_raw + T.c0);
+                const double2 *h1 = reinterpret_cast<const double2 *>(Hb + (int64_t)(T.r0 + r + 1) * ldh_raw + T.c0);
+                double2 a[4], b[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const bool in = 2 * lane + 64 * q < T.cols;
+                    a[q] = in ? __ldcs(h0 + lane + 32 * q) : make_double2(0.0, 0.0);
+                    b[q] = (in && two) ? __ldcs(h1 + lane + 32 * q) : make_double2(0.0, 0.0);
+                }
+                const double pi0 = p[row_begin + T.r0 + r];
+                const double pi1 = two ? p[row_begin + T.r0 + r + 1] : 0.0;
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    s0 = fma(a[q].x, pj[q].x, s0);
+                    s0 = fma(a[q].y, pj[q].y, s0);
+                    s1 = fma(b[q].x, pj[q].x, s1);
+                    s1 = fma(b[q].y, pj[q].y, s1);
+                    ca[q].x = fma(a[q].x, pi0, ca[q].x);
+                    ca[q].y = fma(a[q].y, pi0, ca[q].y);
+                    ca[q].x = fma(b[q].x, pi1, ca[q].x);
+                    ca[q].y = fma(b[q].y, pi1, ca[q].y);
+                }
+                // two row sums over 32 lanes: swap halves (xor 16) so lanes < 16 carry row r and
+                // lanes >= 16 row r + 1, then a 4-step tree inside each half
+                const bool hi = lane & 16;
+                const double send = hi ? s0 : s1, keep = hi ? s1 : s0;
+                double v = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) {
+                    ypart[(int64_t)(T.r0 + r) * ldy + T.rslot] = v;
+                    if (pdot) dacc = fma(pi0, v, dacc);
+                }
+                if (lane == 16 && two) {
+                    ypart[(int64_t)(T.r0 + r + 1) * ldy + T.rslot] = v;
+                    if (pdot) dacc = fma(pi1, v, dacc);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c = 2 * lane + 64 * q;
+                if (c < T.cols) {
+                    ypart[(int64_t)(T.cbase + c) * ldy + T.cslot] = ca[q].x;
+                    if (pdot) dacc = fma(pj[q].x, ca[q].x, dacc);
+                }
+                if (c + 1 < T.cols) {
+                    ypart[(int64_t)(T.cbase + c + 1) * ldy + T.cslot] = ca[q].y;
+                    if (pdot) dacc = fma(pj[q].y, ca[q].y, dacc);
+                }
+            }
+        }
+    } else
+#elif IPM_SYM_LDGW > 0
     if (warp > kSymConsumers) {
         const int lw = warp - kSymConsumers - 1;
         const long long r0 = (long long)blockIdx.x * g_ldg_rows, r1 = r0 + g_ldg_rows;
@@ -728,11 +801,13 @@ void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double
     if (mode == 1)
         k_symv_bulk<1><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
                                                              P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
-                                                             dpart, sc, cid, P.sym_keep, sigb_dot, P.ktimer);
+                                                             dpart, sc, cid, P.sym_keep, sigb_dot, P.ktimer, P.H, P.ldh,
+                                                             P.sym_ntma, P.sym_ntiles);
     else
         k_symv_bulk<0><<<grid, kSymThreads, kSymSmem, st>>>(tm, P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
                                                              P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
-                                                             dpart, sc, cid, P.sym_keep, sigb_dot, P.ktimer);
+                                                             dpart, sc, cid, P.sym_keep, sigb_dot, P.ktimer, P.H, P.ldh,
+                                                             P.sym_ntma, P.sym_ntiles);
 }
 
 // Work plan of the symmetric GEMV (kernels.h).  Blocks: every rank's rows cut into kSymB
@@ -811,6 +886,18 @@ void sym_plan_build(int ncols, int nranks, int rank, int grid, SymPlan &pl) {
     for (size_t q = 0; q < zcols.size(); ++q)
         for (int c = 0; c < bsz(zcols[q].first, zcols[q].second); ++c)
             pl.zcol.push_back((int)rb(zcols[q].first) + zcols[q].second * kSymB + c);
+    // Hybrid SYMV (kSymLdgEvery > 0): every k-th off-diagonal own-rank tile is taken out of the TMA
+    // stream and processed whole by the LDG warps (appended after the TMA tiles below)
+    std::vector<SymTile> ltiles;
+    if (kSymLdgEvery > 0) {
+        std::vector<SymTile> keep;
+        int q = 0;
+        for (const SymTile &T : pl.tiles) {
+            if (T.cmode == 1 && (++q % kSymLdgEvery) == 0) ltiles.push_back(T);
+            else keep.push_back(T);
+        }
+        pl.tiles.swap(keep);
+    }
     // Interleaved order (default; IPM_SYM_ORDER=0 restores row-major ranges): CTA b's contiguous
     // range holds the tiles b, b + grid, b + 2 grid, ... of the row-major order, so at any moment
     // all CTAs stream the same few block rows (a shared TLB working set) instead of 148 distant
@@ -865,6 +952,8 @@ void sym_plan_build(int ncols, int nranks, int rank, int grid, SymPlan &pl) {
     }
     pl.ldy = pl.nbg + pl.ycarry_n + (nranks > 1 ? 1 : 0);    // sharded: + the exchanged slot
     pl.ldz = nba + pl.zcarry_n;
+    pl.ntma = (int)pl.tiles.size();
+    pl.tiles.insert(pl.tiles.end(), ltiles.begin(), ltiles.end());
 }
 
 // Exact-symmetry check at create (the symmetric GEMV is only used when H == H^T bitwise).

@@ -104,6 +104,7 @@ struct Prob {
     const struct SymTile *sym_tiles;     // device: the tile list
     double *sym_z;                       // sharded: column parts of other ranks' rows [zrows][ldz]
     int sym_ycarry, sym_ldz, sym_zcarry; // ypart carry base (= nbg), zpart stride and carry base
+    int sym_ntma, sym_ntiles;            // hybrid SYMV: tiles [ntma, ntiles) go to the LDG warps
     int64_t row_begin;                   // global index of local row 0
     // compact quasi-Newton Hessian H = diag(h0) + U diag(w) U^T (compact.cu)
     int hess_compact;

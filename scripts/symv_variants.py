@@ -28,6 +28,7 @@ import hashlib, numpy as np
 rng = np.random.default_rng(1)
 y = qp.op_apply(rng.uniform(0, 3, n), 10.0 ** rng.uniform(-2, 2, q.m), rng.normal(size=n)).cpu().numpy()
 digest = hashlib.sha1(y.tobytes()).hexdigest()[:12]
+np.save("/tmp/symv_y_" + (var or "prod") + ".npy", y)
 reps = 5 if n > 50000 else 20
 g = qp.profile("gemv", reps)
 sp = qp.profile("spmv", reps)
@@ -44,4 +45,13 @@ for var in sys.argv[2:]:
                        check=True, capture_output=True)
         env["IPM_LIB"] = os.path.join(ROOT, "paper_2405_03584_b200", f"libipm_{var}.so")
     r = subprocess.run([sys.executable, "-c", CHILD, wl, var], env=env, capture_output=True, text=True)
-    print(r.stdout.strip() or r.stderr[-1500:], flush=True)
+    line = r.stdout.strip()
+    if line.startswith("{"):
+        import numpy as np
+        d = json.loads(line)
+        ref = "/tmp/symv_y_prod.npy"
+        if var and os.path.exists(ref):
+            y0, y1 = np.load(ref), np.load("/tmp/symv_y_" + var + ".npy")
+            d["max_rel_diff_vs_prod"] = float(np.max(np.abs(y1 - y0)) / np.max(np.abs(y0)))
+        line = json.dumps(d)
+    print(line or r.stderr[-1500:], flush=True)
