@@ -78,7 +78,7 @@ struct Offsets {
     size_t nvec[40];
     size_t mvec[40];
     size_t ypart, part, ATrp, ATcol, ATval, g, l, u, xl, xu, diagH, cnt, bad, gfull, xloc_all;
-    size_t ch0, cw, cs, cspart, chpart, symr, symt, symz, zcol, zvec, zall, hashes, peer;
+    size_t kd, ch0, cw, cs, cspart, chpart, symr, symt, symz, zcol, zvec, zall, hashes, peer;
     int n_nvec, n_mvec;
     int nchunk;
 };
@@ -123,6 +123,7 @@ Offsets plan(int64_t nloc, int64_t ncols, int64_t m, int64_t nnz_loc, int nranks
     o.l = L.take(sizeof(double) * std::max<int64_t>(m, 1));
     o.u = L.take(sizeof(double) * std::max<int64_t>(m, 1));
     o.diagH = L.take(sizeof(double) * std::max<int64_t>(nloc, 1));
+    o.kd = L.take(ncols <= kWarpMaxN && nranks == 1 ? sizeof(double) * kWarpMaxN * kWarpMaxN : 256);
     o.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(128, m));
     o.cnt = L.take(sizeof(int) * (size_t)o.nchunk * std::max<int64_t>(nloc, 1));
     o.bad = L.take(sizeof(unsigned long long));
@@ -592,12 +593,30 @@ struct PcgOut {
     double relres = 0.0;
     bool stalled = false;
     int restarts = 0;
+    bool deferred = false;   // one-warp path launched without a host sync: collect at the next sync
 };
+
+// Results of a deferred one-warp PCG solve from the host copy of the scalars (after a sync).
+ipm_status pcg_collect(ipm_ctx *ctx, PcgOut &out) {
+    if (!out.deferred) return IPM_OK;
+    out.deferred = false;
+    const Scalars &h = *ctx->hsc;
+    out.iters = h.it;
+    out.relres = h.rhs2 > 0 ? std::sqrt(h.res2 / h.rhs2) : 0.0;
+    out.stalled = h.stalled != 0;
+    out.restarts = (int)h.restarts;
+    if (h.breakdown)
+        return fail(ctx, IPM_ERR_PCG_BREAKDOWN, "PCG breakdown at iteration %lld (p^T K p = %g)", (long long)h.it, h.pKp);
+    if (!std::isfinite(h.res2)) return fail(ctx, IPM_ERR_NONFINITE, "non-finite PCG residual");
+    return IPM_OK;
+}
 
 // Solve K dx = rhs (V.rhs -> V.dx) with the current diagonals; Minv already set.
 // fixed > 0 (test hook ipm_pcg_iterate): exactly `fixed` iterations from x0 = 0 — no stopping
 // test (tolerance 0), no true-residual confirmation, no restart; same kernels and launch path.
-ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) {
+// defer: the one-warp path (n <= kWarpMaxN) returns without a host sync, out.deferred set; the
+// caller runs pcg_collect after its next sync_scalars.
+ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0, bool defer = false) {
     const Prob &P = ctx->P;
     Vecs &V = ctx->V;
     int64_t maxit = ctx->opt.pcg_max_iter > 0 ? ctx->opt.pcg_max_iter : 10 * (int64_t)ctx->n;
@@ -626,6 +645,14 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) 
     const bool graph = ctx->opt.use_graph && (!ctx->sharded || ctx->peer_on) && !small;
     if (graph) TRY(build_graph(ctx));
     out = PcgOut{};
+    if (small && pcg_warp_path(P)) {               // the whole solve, restarts included, in one warp
+        ctx->launches += launch_pcg_small(P, V, ctx->sc, V.dx, V.rhs, fixed == 0 ? 1 : 0, ctx->st);
+        CKL();
+        out.deferred = true;
+        if (defer) return IPM_OK;
+        TRY(sync_scalars(ctx));
+        return pcg_collect(ctx, out);
+    }
     int64_t it_prev = 0;
     // kernels per PCG iteration (sharded peer plane: + 2 per exchange, + zfold)
     const int per_it = (ctx->fused_p ? 2 : 3) + (P.m > 0 ? 2 : 0) +
@@ -642,8 +669,7 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0) 
             CKL();
         }
         if (small) {
-            launch_pcg_small(P, V, ctx->sc, V.dx, ctx->st);
-            ctx->launches += 1;
+            ctx->launches += launch_pcg_small(P, V, ctx->sc, V.dx, V.rhs, 0, ctx->st);
             TRY(sync_scalars(ctx));
         } else if (graph) {
             CK(cudaGraphLaunch(ctx->gexec, ctx->st));
@@ -733,12 +759,14 @@ ipm_status direction(ipm_ctx *ctx, double mu, int mode, double smu, double tau, 
     ctx->launches += 1 + (P.m > 0 ? 1 : 0);
     CKL();
     CK(cudaEventRecord(ctx->ev[2], ctx->st));
-    TRY(pcg_solve(ctx, pcg_rtol(ctx->opt, mu), po));
+    TRY(pcg_solve(ctx, pcg_rtol(ctx->opt, mu), po, 0, true));
     CK(cudaEventRecord(ctx->ev[3], ctx->st));
-    float ms = 0.f;
-    CK(cudaEventSynchronize(ctx->ev[3]));
-    CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
-    tpcg += ms;
+    if (!po.deferred) {
+        float ms = 0.f;
+        CK(cudaEventSynchronize(ctx->ev[3]));
+        CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+        tpcg += ms;
+    }
     const double *dxf = nullptr;
     TRY(gather(ctx, V.dx, &dxf));
     launch_spmv(P, dxf, nullptr, V.Adx, nullptr, ctx->sc, 0, 0, ctx->st);
@@ -795,6 +823,14 @@ ipm_status solve_impl(ipm_ctx *ctx) {
     ipm_status status = IPM_NOT_CONVERGED;
     const bool pc = o.predictor_corrector && ctx->nbounds > 0;
     int k = 0;
+    // a deferred (one-warp) PCG solve is read back at the next sync point
+    auto collect = [&](PcgOut &po) -> ipm_status {
+        if (!po.deferred) return IPM_OK;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+        tpcg += ms;
+        return pcg_collect(ctx, po);
+    };
     DBG("solve start: n=%d m=%d mu0=%.3e kkt=%.3e\n", ctx->P.n, ctx->P.m, mu, kkt_inf(*ctx->hsc));
     for (k = 1; k <= o.max_ipm_iter; ++k) {
         launch_sigma(ctx->P, ctx->V, ctx->G, ctx->st);
@@ -811,6 +847,7 @@ ipm_status solve_impl(ipm_ctx *ctx) {
             TRY(xcombine(ctx, X_MUAFF));
             ctx->launches += 2 * (1 + (ctx->P.m > 0 ? 1 : 0));
             TRY(sync_scalars(ctx));
+            TRY(collect(po));
             const double nb = (double)ctx->nbounds;
             const double mu_cur = ctx->hsc->sum_ls / nb;
             const double mu_aff = ctx->hsc->muaff / nb;
@@ -827,6 +864,8 @@ ipm_status solve_impl(ipm_ctx *ctx) {
         }
         TRY(residuals(ctx, pc ? 0.0 : mu));
         TRY(sync_scalars(ctx));
+        TRY(collect(po));
+        TRY(collect(po2));
         const Scalars &h = *ctx->hsc;
         const int64_t its = po.iters + po2.iters;
         S.pcg_iters_total += its;
@@ -1130,6 +1169,7 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         P.xl = xld;
         P.xu = xud;
         P.diagH = reinterpret_cast<double *>(ctx->ws + o.diagH);
+        P.Kd = reinterpret_cast<double *>(ctx->ws + o.kd);
         int64_t *ATrp = reinterpret_cast<int64_t *>(ctx->ws + o.ATrp);
         int *ATcol = reinterpret_cast<int *>(ctx->ws + o.ATcol);
         double *ATval = reinterpret_cast<double *>(ctx->ws + o.ATval);

@@ -153,8 +153,13 @@ void launch_pcg_iteration(const Prob &P, const Vecs &V, int G, int ncb, int gemv
                           bool fused_p = false);
 void launch_pcg_restart(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st);
+constexpr int kWarpMaxN = 64;       // one-warp PCG on an assembled K at or below this size
 constexpr int kSmallN = 256;        // single-CTA PCG loop below this size (launch-latency bound)
-void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cudaStream_t st);
+// one-warp path (n <= kWarpMaxN, K assembled): also confirms the true residual and restarts in the
+// kernel when check = 1 (sc->res2 / restarts / stalled); the single-CTA path leaves that to the host
+bool pcg_warp_path(const Prob &P);
+int launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, const double *rhs, int check,
+                     cudaStream_t st);
 void launch_pcg_update(const Prob &P, const Vecs &V, int G, int ncb, Scalars *sc, double *x, cudaStream_t st);
 
 // shard.cu

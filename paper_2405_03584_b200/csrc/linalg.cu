@@ -775,8 +775,10 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
 
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
                       int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot) {
-#if IPM_SYM_LDGW > 0
-    {
+#if IPM_SYM_LDGW > 0 && IPM_SYM_LDG_EVERY == 0
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusNone) {      // the symbols persist into captured launches
         const char *e = getenv("IPM_SYM_LDGROWS");
         const long long rows = e ? atoll(e) : 34, ldh = P.ldh, n = P.ncols;
         const double *h = P.H;

@@ -784,103 +784,104 @@ k_pcg_small(int n, int m, const double *__restrict__ H, int64_t ldh, const int64
 
 
 // ------------------------------------------------------------- tiny problems: one WARP
-// For n <= 64 (C1: n = 50, m = 20) the PCG loop runs in ONE warp with every operand in shared
-// memory: lane l owns rows l and l + 32 of every x-space vector, rows l, l + 32, ... of A; the
-// phases are separated by __syncwarp only and every reduction is a 5-step xor-shuffle tree —
-// no block barriers (k_pcg_small's 6 per iteration).  Same recurrence and stopping rule.
-constexpr int kWarpMaxN = 64;
+// For n <= kWarpMaxN (C1: n = 50, m = 20) the PCG runs on the ASSEMBLED condensed matrix
+//   K = H + A^T Sigma_c A + Sigma_b                      (the Schur complement of eq:2x2_reduced)
+// — at this size forming K costs less than a handful of matrix-free iterations, and an iteration
+// becomes one dense n x n product from shared memory with no sparse index chasing (P:263-268 still
+// holds: the Jacobi preconditioner is diag(K), unchanged).  k_form_K writes K once per PCG launch
+// (one CTA per row i, thread j: (A^T Sigma_c A)_ij summed over the nonzeros A_ki in ascending k, each
+// term sigma_k (A_ki A_kj) — a commutative product, so K is bitwise symmetric), then k_pcg_warp runs
+// the whole loop in ONE warp: lane l owns rows l and l + 32, reads column i of K (= row i, K
+// symmetric) with consecutive lanes on consecutive words, p broadcast from shared memory; the phases
+// are separated by __syncwarp only and every reduction is a 5-step xor-shuffle tree.
+__global__ void __launch_bounds__(kWarpMaxN)
+k_form_K(int n, const double *__restrict__ H, int64_t ldh, const int64_t *__restrict__ Arp,
+         const int *__restrict__ Acol, const double *__restrict__ Aval, const int64_t *__restrict__ ATrp,
+         const int *__restrict__ ATcol, const double *__restrict__ ATval, const double *__restrict__ sigb,
+         const double *__restrict__ sigc, double *__restrict__ K) {
+    __shared__ double arow[kWarpMaxN];
+    const int i = blockIdx.x, j = threadIdx.x;
+    double acc = 0.0;
+    for (int64_t e = ATrp[i]; e < ATrp[i + 1]; ++e) {
+        const int k = ATcol[e];
+        arow[j] = 0.0;                                   // row k of A, dense
+        __syncthreads();
+        for (int64_t q = Arp[k] + j; q < Arp[k + 1]; q += kWarpMaxN) arow[Acol[q]] = Aval[q];
+        __syncthreads();
+        acc = fma(sigc[k], ATval[e] * arow[j], acc);
+        __syncthreads();
+    }
+    if (j < n) K[(int64_t)i * kWarpMaxN + j] = (H[(int64_t)i * ldh + j] + acc) + (i == j ? sigb[i] : 0.0);
+}
 
 __global__ void __launch_bounds__(32)
-k_pcg_warp(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_t *__restrict__ Arp,
-           const int *__restrict__ Acol, const double *__restrict__ Aval, const int64_t *__restrict__ ATrp,
-           const int *__restrict__ ATcol, const double *__restrict__ ATval, const double *__restrict__ sigb,
-           const double *__restrict__ sigc, const double *__restrict__ Minv, double *x, double *r, double *z,
-           double *p, double *t, double *y, Scalars *sc, int64_t nnz) {
+k_pcg_warp(int n, int m, const double *__restrict__ K, const int64_t *__restrict__ Arp,
+           const int *__restrict__ Acol, const double *__restrict__ Aval, const double *__restrict__ sigc,
+           const double *__restrict__ Minv, const double *__restrict__ rhs, double *x, double *r, double *z,
+           double *p, double *t, double *y, Scalars *sc, int check) {
     extern __shared__ __align__(16) double sm[];
-    if (sc->done) return;
     const int l = threadIdx.x;
-    const int hs = n | 1;                          // odd row stride: conflict-free column access
-    double *sp = sm, *st = sm + kWarpMaxN, *sH = st + m, *scg = sH + (int64_t)n * hs, *aval = scg + m,
-           *atval = aval + nnz;
-    int *arp = reinterpret_cast<int *>(atval + nnz), *acol = arp + (m + 1), *atrp = acol + nnz, *atcol = atrp + (n + 1);
-    for (int i = 0; i < n; ++i)                    // row by row: no 64-bit index division
-        for (int j = l; j < n; j += 32) sH[(int64_t)i * hs + j] = H[(int64_t)i * ldh + j];
-    for (int i = l; i < m; i += 32) scg[i] = sigc[i];
-    for (int i = l; i <= m; i += 32) arp[i] = (int)Arp[i];
-    for (int i = l; i <= n; i += 32) atrp[i] = (int)ATrp[i];
-    for (int64_t k = l; k < nnz; k += 32) {
-        aval[k] = Aval[k];
-        acol[k] = Acol[k];
-        atval[k] = ATval[k];
-        atcol[k] = ATcol[k];
+    double *sp = sm, *sK = sm + kWarpMaxN;
+    for (int i = 0; i < n; ++i) {
+        sK[i * kWarpMaxN + l] = (l < n) ? K[(int64_t)i * kWarpMaxN + l] : 0.0;
+        sK[i * kWarpMaxN + l + 32] = (l + 32 < n) ? K[(int64_t)i * kWarpMaxN + l + 32] : 0.0;
     }
+    sp[l] = 0.0;
+    sp[l + 32] = 0.0;
     // this lane's rows (registers): i0 = l, i1 = l + 32
     const int i0 = l, i1 = l + 32;
     const bool h0 = i0 < n, h1 = i1 < n;
     double p0 = h0 ? p[i0] : 0.0, p1 = h1 ? p[i1] : 0.0, r0 = h0 ? r[i0] : 0.0, r1 = h1 ? r[i1] : 0.0;
     double z0 = h0 ? z[i0] : 0.0, z1 = h1 ? z[i1] : 0.0, x0 = h0 ? x[i0] : 0.0, x1 = h1 ? x[i1] : 0.0;
-    const double m0 = h0 ? Minv[i0] : 0.0, m1 = h1 ? Minv[i1] : 0.0, b0 = h0 ? sigb[i0] : 0.0,
-                 b1 = h1 ? sigb[i1] : 0.0;
+    const double m0 = h0 ? Minv[i0] : 0.0, m1 = h1 ? Minv[i1] : 0.0;
     double y0 = 0.0, y1 = 0.0;
     double rho = sc->rho, rho_old = sc->rho_old, rr = sc->rr, pkp = 0.0, alpha_last = 0.0;
     int64_t it = sc->it, it_rs = sc->it_rs;
     const double tol2 = sc->tol2;
     const int64_t maxit = sc->maxit;
-    int breakdown = 0;
-    // (H p)_i + (A^T t)_i with four independent FMA chains (fp64 FMA latency, not throughput,
-    // bounds a lane's row), combined in a fixed order
-    auto row_dot = [&](int i) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-        const double *__restrict__ h = sH + (int64_t)i * hs;
+    int breakdown = (int)sc->breakdown, done = (int)sc->done, stalled = 0, restarts = 0;
+    double res2 = 0.0;
+    const int n4 = n & ~3;
+    // (K v)_i for this lane's rows from v in sp: four FMA chains per row over j mod 4, fixed order
+    auto kmul = [&](double &o0, double &o1) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
         int j = 0;
-        for (; j + 7 < n; j += 8) {                // 8 chains: 16 shared loads in flight per lane
-            a0 = fma(h[j], sp[j], a0);
-            a1 = fma(h[j + 1], sp[j + 1], a1);
-            a2 = fma(h[j + 2], sp[j + 2], a2);
-            a3 = fma(h[j + 3], sp[j + 3], a3);
-            e0 = fma(h[j + 4], sp[j + 4], e0);
-            e1 = fma(h[j + 5], sp[j + 5], e1);
-            e2 = fma(h[j + 6], sp[j + 6], e2);
-            e3 = fma(h[j + 7], sp[j + 7], e3);
+#pragma unroll 4
+        for (; j < n4; j += 4) {
+            const double2 pa = *reinterpret_cast<const double2 *>(sp + j);
+            const double2 pb = *reinterpret_cast<const double2 *>(sp + j + 2);
+            const double *kr = sK + j * kWarpMaxN;
+            a0 = fma(kr[l], pa.x, a0);
+            c0 = fma(kr[l + 32], pa.x, c0);
+            a1 = fma(kr[kWarpMaxN + l], pa.y, a1);
+            c1 = fma(kr[kWarpMaxN + l + 32], pa.y, c1);
+            a2 = fma(kr[2 * kWarpMaxN + l], pb.x, a2);
+            c2 = fma(kr[2 * kWarpMaxN + l + 32], pb.x, c2);
+            a3 = fma(kr[3 * kWarpMaxN + l], pb.y, a3);
+            c3 = fma(kr[3 * kWarpMaxN + l + 32], pb.y, c3);
         }
-        for (; j < n; ++j) a0 = fma(h[j], sp[j], a0);
-        a0 += e0;
-        a1 += e1;
-        a2 += e2;
-        a3 += e3;
-        int k = atrp[i];
-        const int ke = atrp[i + 1];
-        for (; k + 1 < ke; k += 2) {
-            a1 = fma(atval[k], st[atcol[k]], a1);
-            a3 = fma(atval[k + 1], st[atcol[k + 1]], a3);
+        for (; j < n; ++j) {
+            a0 = fma(sK[j * kWarpMaxN + l], sp[j], a0);
+            c0 = fma(sK[j * kWarpMaxN + l + 32], sp[j], c0);
         }
-        if (k < ke) a2 = fma(atval[k], st[atcol[k]], a2);
-        return (a0 + a1) + (a2 + a3);
+        o0 = h0 ? (a0 + a1) + (a2 + a3) : 0.0;
+        o1 = h1 ? (c0 + c1) + (c2 + c3) : 0.0;
     };
     __syncwarp();
-    for (;;) {
+    // check = 1: after the recurrence stops, the true residual rhs - K x confirms it and a
+    // failed check restarts from it — the host loop of pcg_solve, run here with the same limits
+    // (restart rounds <= 8, the iteration limit), so a tiny solve needs no host round trip.
+    for (int round = 0; !breakdown; ++round) {
+    while (!done) {
         const bool first = (it_rs == 0);
         const double beta = first ? 0.0 : rho / rho_old;
         p0 = first ? z0 : fma(beta, p0, z0);
         p1 = first ? z1 : fma(beta, p1, z1);
-        if (h0) sp[i0] = p0;
-        if (h1) sp[i1] = p1;
+        sp[i0] = p0;                               // 0 beyond n: the padded K columns read zeros
+        sp[i1] = p1;
         __syncwarp();
-        for (int i = l; i < m; i += 32) {          // t = sig_c o (A p), two chains per row
-            double a = 0.0, c = 0.0;
-            int k = arp[i];
-            const int ke = arp[i + 1];
-            for (; k + 1 < ke; k += 2) {
-                a = fma(aval[k], sp[acol[k]], a);
-                c = fma(aval[k + 1], sp[acol[k + 1]], c);
-            }
-            if (k < ke) a = fma(aval[k], sp[acol[k]], a);
-            st[i] = scg[i] * (a + c);
-        }
-        __syncwarp();
-        y0 = h0 ? fma(b0, p0, row_dot(i0)) : 0.0;
-        y1 = h1 ? fma(b1, p1, row_dot(i1)) : 0.0;
-        // p^T K p = p^T y (y = H p + sig_b p + A^T t, as k_pcg_small), xor-tree over the lanes
+        kmul(y0, y1);                              // y = K p
+        // p^T K p = p^T y, xor-tree over the lanes
         double d = fma(p0, y0, p1 * y1);
         d = warp_sum(d);
         pkp = d;
@@ -911,9 +912,39 @@ k_pcg_warp(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_
             breakdown = 1;
             break;
         }
-        if (rr <= tol2 || it >= maxit) break;
-        __syncwarp();                              // st / sp reads done before the next overwrite
+        done = (rr <= tol2 || it >= maxit) ? 1 : 0;
+        __syncwarp();                              // sp reads done before the next overwrite
     }
+    if (breakdown || !check) break;
+    // true residual r = rhs - K x with the same K
+    __syncwarp();
+    sp[i0] = x0;
+    sp[i1] = x1;
+    __syncwarp();
+    double kx0, kx1;
+    kmul(kx0, kx1);
+    const double rt0 = h0 ? rhs[i0] - kx0 : 0.0, rt1 = h1 ? rhs[i1] - kx1 : 0.0;
+    res2 = warp_sum(fma(rt1, rt1, rt0 * rt0));
+    if (!finite_d(res2) || res2 <= tol2) break;   // non-finite: reported by the host (IPM_ERR_NONFINITE)
+    if (it >= maxit || round >= 8) {
+        stalled = 1;
+        break;
+    }
+    ++restarts;                                    // restart from the true residual (k_pcg_restart)
+    r0 = rt0;
+    r1 = rt1;
+    z0 = m0 * r0;
+    z1 = m1 * r1;
+    const double trz = warp_sum(fma(r1, z1, r0 * z0)), trr = warp_sum(fma(r1, r1, r0 * r0));
+    rho = rho_old = trz;
+    rr = trr;
+    it_rs = 0;
+    done = (rr <= tol2 || it >= maxit) ? 1 : 0;
+    __syncwarp();
+    }
+    __syncwarp();
+    sp[i0] = p0;                                   // t below is formed from the last direction
+    sp[i1] = p1;
     if (h0) {
         p[i0] = p0; r[i0] = r0; z[i0] = z0; x[i0] = x0; y[i0] = y0;
     }
@@ -921,7 +952,12 @@ k_pcg_warp(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_
         p[i1] = p1; r[i1] = r1; z[i1] = z1; x[i1] = x1; y[i1] = y1;
     }
     __syncwarp();
-    for (int i = l; i < m; i += 32) t[i] = st[i];
+    // t = Sigma_c (A p) of the last direction (the matrix-free loops leave it in t as well)
+    for (int i = l; i < m; i += 32) {
+        double a = 0.0;
+        for (int64_t k = Arp[i]; k < Arp[i + 1]; ++k) a = fma(Aval[k], sp[Acol[k]], a);
+        t[i] = sigc[i] * a;
+    }
     if (l == 0) {
         sc->rho = rho;
         sc->rho_old = rho_old;
@@ -931,14 +967,14 @@ k_pcg_warp(int n, int m, const double *__restrict__ H, int64_t ldh, const int64_
         sc->it = it;
         sc->it_rs = it_rs;
         sc->done = 1;
+        sc->res2 = res2;
+        sc->restarts = restarts;
+        sc->stalled = stalled;
         if (breakdown) sc->breakdown = 1;
     }
 }
 
-static size_t warp_smem_bytes(const Prob &P) {
-    const size_t n = P.n, m = P.m, nnz = P.nnz;
-    return 8 * (kWarpMaxN + m + n * (n | 1) + m + 2 * nnz) + 4 * (m + 1 + n + 1 + 2 * nnz);
-}
+static size_t warp_smem_bytes() { return 8 * (kWarpMaxN + kWarpMaxN * kWarpMaxN); }
 
 static int pcg_warp_enabled() {
     static int e = -1;
@@ -952,16 +988,20 @@ static int pcg_warp_enabled() {
 cudaError_t configure_pcg_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_pcg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmemMax);
     const cudaError_t e2 = cudaFuncSetAttribute(k_pcg_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)kSmallSmemMax);
+                                                (int)warp_smem_bytes());
     return e != cudaSuccess ? e : e2;
 }
 
-void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cudaStream_t st) {
-    if (pcg_warp_enabled() && P.n <= kWarpMaxN && warp_smem_bytes(P) <= kSmallSmemMax) {
-        k_pcg_warp<<<1, 32, warp_smem_bytes(P), st>>>(P.n, P.m, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol,
-                                                       P.ATval, V.sig_b, V.sig_c, V.Minv, x, V.pr, V.pz, V.pp, V.pt,
-                                                       V.py, sc, P.nnz);
-        return;
+bool pcg_warp_path(const Prob &P) { return pcg_warp_enabled() && P.n <= kWarpMaxN && P.Kd; }
+
+int launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, const double *rhs, int check,
+                     cudaStream_t st) {
+    if (pcg_warp_path(P)) {
+        k_form_K<<<P.n, kWarpMaxN, 0, st>>>(P.n, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol, P.ATval,
+                                           V.sig_b, V.sig_c, P.Kd);
+        k_pcg_warp<<<1, 32, warp_smem_bytes(), st>>>(P.n, P.m, P.Kd, P.Arp, P.Acol, P.Aval, V.sig_c, V.Minv, rhs,
+                                                      x, V.pr, V.pz, V.pp, V.pt, V.py, sc, check);
+        return 2;
     }
     size_t bytes = 7 * (size_t)P.n * 8;
     const int t_in = (bytes + (size_t)P.m * 8 <= kSmallSmemMax) ? 1 : 0;
@@ -975,6 +1015,7 @@ void launch_pcg_small(const Prob &P, const Vecs &V, Scalars *sc, double *x, cuda
     k_pcg_small<<<1, kSmallThreads, bytes, st>>>(P.n, P.m, P.H, P.ldh, P.Arp, P.Acol, P.Aval, P.ATrp, P.ATcol,
                                                  P.ATval, V.sig_b, V.sig_c, V.Minv, x, V.pr, V.pz, V.pp, V.pt, V.py,
                                                  sc, t_in, h_in, a_in, P.nnz);
+    return 1;
 }
 
 void launch_pcg_p(const Prob &P, const Vecs &V, Scalars *sc, cudaStream_t st) {
@@ -1259,6 +1300,7 @@ void preload_pcg() {
     touch_kernel(k_pcg_update_fp<4, true, 1024>); touch_kernel(k_pcg_update_fp<8, true, 1024>);
     touch_kernel(k_pcg_small);
     touch_kernel(k_pcg_warp);
+    touch_kernel(k_form_K);
     touch_kernel(k_spmvT<4>); touch_kernel(k_spmvT<8>); touch_kernel(k_spmvT<16>); touch_kernel(k_spmvT<32>);
     touch_kernel(k_cg_prime); touch_kernel(k_cg_update<4>); touch_kernel(k_cg_update<8>);
     touch_kernel(k_cg_update<16>); touch_kernel(k_cg_update<32>);

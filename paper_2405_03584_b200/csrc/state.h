@@ -29,6 +29,8 @@ struct Scalars {
     int64_t maxit;
     int64_t done;      // 1 = stop the loop (converged or limit or breakdown)
     int64_t breakdown; // 1 = p^T K p <= 0 or non-finite
+    int64_t restarts;  // one-warp PCG (n <= kWarpMaxN): true-residual restarts taken in the kernel
+    int64_t stalled;   // one-warp PCG: stopped at the iteration / restart limit above tolerance
     // --- IPM -----------------------------------------------------------------------------
     double sum_ls_m, sum_ls;     // sum lam*s (init / mu updates)
     double rH_max_m, rH_max;     // (m-part unused slot kept for symmetry)
@@ -115,6 +117,7 @@ struct Prob {
     double *cs, *cspart, *chpart;   // s = U^T p (ldu), per-CTA column partials, per-CTA h0 p^2 partials
     int aug;               // 1: PCG on the doubly augmented system eq:2x2_augmented
     int ktimer;            // 1: the PCG-mode operator kernel times its launches (opt.kernel_timer)
+    double *Kd;            // n <= kWarpMaxN: the condensed K assembled densely (kWarpMaxN x kWarpMaxN)
 };
 
 // Iterate, residuals and per-IPM-iteration work vectors (masked full-length layout).
