@@ -131,6 +131,57 @@ __device__ __forceinline__ int ld_keep(const int *p, uint64_t pol) {
     return v;
 }
 
+__device__ __forceinline__ double2 ld_keep2(const double *p, uint64_t pol) {     // 16-B aligned
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int2 ld_keep2(const int *p, uint64_t pol) {           // 8-B aligned
+    int2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Dot of one CSR row with a dense vector x by one group of G lanes, 16-B column-pair loads
+// (experiment IPM_SPMV_VEC): an odd leading entry is taken by lane 0 first, then lane l folds the
+// pairs starting at a + 2l, a + 2l + 2G, ... (four in flight per trip), then an odd trailing
+// entry — a fixed order for a given row and G.
+template <int G>
+__device__ __forceinline__ double row_dot_pairs(const int *__restrict__ col, const double *__restrict__ val,
+                                                const double *__restrict__ x, int64_t s, int64_t e, int gl,
+                                                uint64_t pol) {
+    double acc = 0.0;
+    if ((s & 1) && s < e) {
+        if (gl == 0) acc = ld_keep(val + s, pol) * __ldg(x + ld_keep(col + s, pol));
+        ++s;
+    }
+    int64_t k = s + 2 * gl;
+    for (; k + 1 + 6 * G < e; k += 8 * G) {
+        const int2 c0 = ld_keep2(col + k, pol), c1 = ld_keep2(col + k + 2 * G, pol);
+        const int2 c2 = ld_keep2(col + k + 4 * G, pol), c3 = ld_keep2(col + k + 6 * G, pol);
+        const double2 w0 = ld_keep2(val + k, pol), w1 = ld_keep2(val + k + 2 * G, pol);
+        const double2 w2 = ld_keep2(val + k + 4 * G, pol), w3 = ld_keep2(val + k + 6 * G, pol);
+        const double x0 = __ldg(x + c0.x), y0 = __ldg(x + c0.y), x1 = __ldg(x + c1.x), y1 = __ldg(x + c1.y);
+        const double x2 = __ldg(x + c2.x), y2 = __ldg(x + c2.y), x3 = __ldg(x + c3.x), y3 = __ldg(x + c3.y);
+        acc = fma(w0.x, x0, acc);
+        acc = fma(w0.y, y0, acc);
+        acc = fma(w1.x, x1, acc);
+        acc = fma(w1.y, y1, acc);
+        acc = fma(w2.x, x2, acc);
+        acc = fma(w2.y, y2, acc);
+        acc = fma(w3.x, x3, acc);
+        acc = fma(w3.y, y3, acc);
+    }
+    for (; k + 1 < e; k += 2 * G) {
+        const int2 c = ld_keep2(col + k, pol);
+        const double2 w = ld_keep2(val + k, pol);
+        acc = fma(w.x, __ldg(x + c.x), acc);
+        acc = fma(w.y, __ldg(x + c.y), acc);
+    }
+    if (k < e) acc = fma(ld_keep(val + k, pol), __ldg(x + ld_keep(col + k, pol)), acc);
+    return acc;
+}
+
 // Device-side launch timer (ns, %globaltimer): the PCG's dominant kernel records the
 // earliest CTA start and, in its last CTA, adds (end - start) to a running sum, so bench.py
 // reads the kernel's average launch duration over the timed region without splitting the

@@ -372,6 +372,14 @@ __device__ __forceinline__ void consumers_sync() {      // named barrier 1: cons
 
 __device__ __forceinline__ void tma_2d_g2s(void *dst, const CUtensorMap *tmap, int x, int y, uint64_t *bar,
                                            uint64_t pol) {
+#ifdef IPM_SYM_NOHINT       // experiment: no L2 cache policy on the H boxes
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+    return;
+#endif
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
@@ -395,9 +403,16 @@ bool make_sym_tensor_map(const Prob &P, void *out) {
     const cuuint64_t strides[1] = {(cuuint64_t)P.ldh * sizeof(double)};
     const cuuint32_t box[2] = {(cuuint32_t)kSymB, (cuuint32_t)kSymSR};
     const cuuint32_t estr[2] = {1, 1};
+#ifndef IPM_SYM_L2P
+#define IPM_SYM_L2P 3      // experiment switch: 0 none, 1 64 B, 2 128 B, 3 256 B L2 promotion
+#endif
+    const CUtensorMapL2promotion l2p = IPM_SYM_L2P == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : IPM_SYM_L2P == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                       : IPM_SYM_L2P == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     CUresult r = encode(reinterpret_cast<CUtensorMap *>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, P.H, dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2p,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -773,6 +788,189 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
     if (MODE == 1) TL_END(sc, 2);
 }
 
+// ------------------------------------------- symmetric GEMV, register (LDG) streaming variant
+// Same work plan, tile semantics and ypart slots as k_symv_bulk, but H goes straight from HBM
+// into registers: 16 warps per CTA, warp w owns rows 2w and 2w + 1 of every 32-row strip, lane l
+// columns 2l + 64q + {0, 1} (q < 4) — four coalesced 16-B loads per row.  The next strip's loads
+// are issued before the current strip is reduced (two strips in flight per warp).  Row parts are
+// reduced in registers (two rows per 5-step shuffle tree); column parts accumulate per warp over
+// the tile's strips and are combined across the 16 warps through shared memory ONE strip later,
+// after the following loads are in flight (double-buffered, one named barrier per tile), in warp
+// order — deterministic.
+constexpr int kLdgWarps = 16;
+constexpr int kLdgThreads = 32 * kLdgWarps;
+constexpr size_t kLdgSmem = 2ull * kLdgWarps * kSymB * 8;
+static_assert(kLdgWarps * 2 == kSymSR, "two strip rows per warp");
+
+struct LdgUnit {
+    int t, sidx;          // tile, strip (t > tlast: none)
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kLdgThreads, 1)
+k_symv_ldg(const SymTile *__restrict__ tiles, const SymRange *__restrict__ ranges, const double *__restrict__ p,
+           int64_t row_begin, const double *__restrict__ pdot, double *__restrict__ ypart, int ldy, int ycarry,
+           double *__restrict__ zpart, int ldz, int zcarry, double *__restrict__ dpart, Scalars *sc, int cid,
+           const double *__restrict__ sigb_dot, int timed, const double *__restrict__ H, int64_t ldh) {
+    extern __shared__ __align__(16) double cbuf[];        // [2][kLdgWarps][kSymB] column partials
+    __shared__ double red[kLdgWarps];
+    if (MODE == 1 && sc->done) return;
+    if (MODE == 1 && timed) ktimer_start(&sc->kt_neg);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const SymRange rg = ranges[blockIdx.x];
+    const int tlast = rg.s1 > 0 ? rg.t1 : rg.t1 - 1;
+    auto strips_end = [&](int t, const SymTile &T) { return (t == rg.t1) ? rg.s1 : (T.rows + kSymSR - 1) / kSymSR; };
+    double dacc = 0.0;
+    // loads of one strip: rows r0 = 2w, r1 = 2w + 1 of the strip, this lane's 8 columns
+    double2 h0[4], h1[4], n0[4], n1[4];
+    double pi0 = 0.0, pi1 = 0.0, npi0 = 0.0, npi1 = 0.0;
+    auto load = [&](const SymTile &T, int sidx, double2 (&a)[4], double2 (&b)[4], double &qa, double &qb) {
+        const int r = sidx * kSymSR + 2 * warp;
+        const bool ok0 = r < T.rows, ok1 = r + 1 < T.rows;
+        const double *row0 = H + (int64_t)(T.r0 + r) * ldh + T.c0;
+        const double *row1 = row0 + ldh;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = 2 * lane + 64 * q;
+            if (c + 1 < T.cols) {
+                a[q] = ok0 ? __ldcs(reinterpret_cast<const double2 *>(row0 + c)) : make_double2(0.0, 0.0);
+                b[q] = ok1 ? __ldcs(reinterpret_cast<const double2 *>(row1 + c)) : make_double2(0.0, 0.0);
+            } else if (c < T.cols) {                        // odd tail column
+                a[q] = make_double2(ok0 ? __ldcs(row0 + c) : 0.0, 0.0);
+                b[q] = make_double2(ok1 ? __ldcs(row1 + c) : 0.0, 0.0);
+            } else {
+                a[q] = b[q] = make_double2(0.0, 0.0);
+            }
+        }
+        const int64_t gi = row_begin + T.r0 + r;
+        qa = ok0 ? __ldg(p + gi) : 0.0;
+        qb = ok1 ? __ldg(p + gi + 1) : 0.0;
+    };
+    // column-part flush: colacc of this warp -> cbuf[f & 1][warp][.]; reduced one strip later
+    double2 ca[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ca[q] = make_double2(0.0, 0.0);
+    int nflush = 0, pend_t = -1, pend_sa = 0;
+    auto reduce_pending = [&]() {
+        asm volatile("bar.sync 1, %0;" ::"n"(kLdgThreads) : "memory");
+        const SymTile T = tiles[pend_t];
+        const double *buf = cbuf + (size_t)((nflush - 1) & 1) * kLdgWarps * kSymB;
+        if (lane < kSymB / kLdgWarps) {
+            const int c = warp * (kSymB / kLdgWarps) + lane;
+            if (c < T.cols) {
+                double colsum = 0.0;
+#pragma unroll
+                for (int w = 0; w < kLdgWarps; ++w) colsum += buf[w * kSymB + c];
+                if (T.cmode == 1) {
+                    const int slot = (pend_sa == 0) ? T.cslot : ycarry + rg.carry;
+                    ypart[(int64_t)(T.cbase + c) * ldy + slot] = colsum;
+                } else {
+                    const int slot = (pend_sa == 0) ? T.cslot : zcarry + rg.carry;
+                    zpart[(int64_t)(T.cbase + c) * ldz + slot] = colsum;
+                }
+                if (pdot) dacc = fma(__ldg(p + T.c0 + c), colsum, dacc);   // pdot: flag only (as k_symv_bulk)
+            }
+        }
+        pend_t = -1;
+    };
+    LdgUnit cur{rg.t0, rg.s0};
+    if (cur.t <= tlast) {
+        const SymTile T = tiles[cur.t];
+        load(T, cur.sidx, h0, h1, pi0, pi1);
+    }
+    while (cur.t <= tlast) {
+        const SymTile T = tiles[cur.t];
+        const int sa = (cur.t == rg.t0) ? rg.s0 : 0;
+        const int sb = strips_end(cur.t, T);
+        LdgUnit nx{cur.t, cur.sidx + 1};
+        if (nx.sidx >= sb) { nx.t = cur.t + 1; nx.sidx = 0; }
+        if (nx.t <= tlast) {
+            const SymTile TN = tiles[nx.t];
+            load(TN, nx.sidx, n0, n1, npi0, npi1);
+        }
+        if (pend_t >= 0) reduce_pending();               // the next strip's loads are in flight
+        // row parts of rows 2w, 2w + 1 against p_J (L1-resident after the first warp)
+        double s0 = 0.0, s1 = 0.0;
+        double2 pj[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = 2 * lane + 64 * q;
+            pj[q] = (c + 1 < T.cols) ? __ldg(reinterpret_cast<const double2 *>(p + T.c0 + c))
+                                     : make_double2(c < T.cols ? __ldg(p + T.c0 + c) : 0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            s0 = fma(h0[q].x, pj[q].x, s0);
+            s0 = fma(h0[q].y, pj[q].y, s0);
+            s1 = fma(h1[q].x, pj[q].x, s1);
+            s1 = fma(h1[q].y, pj[q].y, s1);
+        }
+        const bool hi = lane & 16;
+        double v = (hi ? s1 : s0) + __shfl_xor_sync(0xffffffffu, hi ? s0 : s1, 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int r = cur.sidx * kSymSR + 2 * warp + (hi ? 1 : 0);
+        if ((lane & 15) == 0 && r < T.rows) {
+            ypart[(int64_t)(T.r0 + r) * ldy + T.rslot] = v;
+            if (pdot) {
+                const double pr = hi ? pi1 : pi0;
+                dacc = fma(pr, v, dacc);
+                if (sigb_dot && T.cmode == 0) dacc = fma(sigb_dot[T.r0 + r] * pr, pr, dacc);
+            }
+        }
+        if (T.cmode != 0) {                              // column parts: rows 2w then 2w + 1
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                ca[q].x = fma(h0[q].x, pi0, ca[q].x);
+                ca[q].y = fma(h0[q].y, pi0, ca[q].y);
+                ca[q].x = fma(h1[q].x, pi1, ca[q].x);
+                ca[q].y = fma(h1[q].y, pi1, ca[q].y);
+            }
+            if (nx.t != cur.t) {                         // last strip of the tile in this range
+                double *buf = cbuf + (size_t)(nflush & 1) * kLdgWarps * kSymB + warp * kSymB;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    reinterpret_cast<double2 *>(buf)[lane + 32 * q] = ca[q];
+                    ca[q] = make_double2(0.0, 0.0);
+                }
+                ++nflush;
+                pend_t = cur.t;
+                pend_sa = sa;
+            }
+        }
+        cur = nx;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            h0[q] = n0[q];
+            h1[q] = n1[q];
+        }
+        pi0 = npi0;
+        pi1 = npi1;
+    }
+    if (pend_t >= 0) reduce_pending();
+    if (pdot == nullptr) return;
+    const double bs = block_sum(dacc, red);
+    if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
+    if (last_block(&sc->counters[cid])) {
+        const double tot = sum_partials(dpart, gridDim.x, red);
+        if (threadIdx.x == 0) {
+            sc->counters[cid] = 0;
+            sc->S_H = tot;
+            if (MODE == 1 && timed) ktimer_stop(&sc->kt_neg, &sc->kt_ns, &sc->kt_count);
+            if (sc->sharded) sc->loc[1] = tot;
+        }
+    }
+}
+
+static int symv_ldg_enabled() {
+    static int e = -1;
+    if (e < 0) {
+        const char *v = getenv("IPM_SYMV_LDG");         // experiment switch: 1 = register-streaming SYMV
+        e = v ? atoi(v) : 0;
+    }
+    return e;
+}
+
 void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double *ypart, double *dpart, Scalars *sc,
                       int grid, int mode, int cid, cudaStream_t st, const double *sigb_dot) {
 #if IPM_SYM_LDGW > 0 && IPM_SYM_LDG_EVERY == 0
@@ -789,6 +987,17 @@ void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double
         cudaStreamSynchronize(st);       // host stack values
     }
 #endif
+    if (symv_ldg_enabled() && (P.ldh % 2) == 0) {
+        if (mode == 1)
+            k_symv_ldg<1><<<grid, kLdgThreads, kLdgSmem, st>>>(P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
+                                                               P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
+                                                               dpart, sc, cid, sigb_dot, P.ktimer, P.H, P.ldh);
+        else
+            k_symv_ldg<0><<<grid, kLdgThreads, kLdgSmem, st>>>(P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
+                                                               P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
+                                                               dpart, sc, cid, sigb_dot, P.ktimer, P.H, P.ldh);
+        return;
+    }
 #ifdef IPM_SYM_LDGSTS
     CUtensorMap raw;
     SymRaw *sr = reinterpret_cast<SymRaw *>(&raw);
@@ -1002,7 +1211,10 @@ k_spmv(int m, const int64_t *__restrict__ rp, const int *__restrict__ col, const
         // in flight together, then folded into the ONE accumulator in k order (so the sum is
         // bitwise the plain loop's)
         int64_t k = s + lane;
-        if (MODE == 1 && keep) {
+        if (keep == 2) {                                 // experiment IPM_SPMV_VEC: pair loads
+            a = row_dot_pairs<32>(col, val, v, s, e, lane, keep_policy());
+            k = e;
+        } else if (MODE == 1 && keep) {
             const uint64_t pol = keep_policy();
             for (; k + 96 < e; k += 128) {
                 const int c0 = ld_keep(col + k, pol), c1 = ld_keep(col + k + 32, pol);
@@ -1073,8 +1285,16 @@ int spmv_keep() {
 
 // (kept for every size: at C5 A and A^T are 480 MB, far above L2, yet the evict_last loads still
 // measured faster than plain ones — SpMV 0.242 vs 0.257 ms, bench 148.7 vs 147.4 PCG it/s,
-// profiles/r02_spmv_keep.txt)
-int spmv_keep_for(const Prob &) { return spmv_keep(); }
+// profiles/r02_spmv_keep.txt).  2 = the column-pair (16-B) load path (IPM_SPMV_VEC=1).
+int spmv_vec() {
+    static int k = -1;
+    if (k < 0) {
+        const char *e = getenv("IPM_SPMV_VEC");
+        k = e ? atoi(e) : 0;
+    }
+    return k;
+}
+int spmv_keep_for(const Prob &) { return spmv_vec() ? 2 : spmv_keep(); }
 
 void launch_spmv(const Prob &P, const double *v, const double *sigc, double *y, double *dpart,
                  Scalars *sc, int mode, int check_done, cudaStream_t st, int max_grid, int block) {
@@ -1427,6 +1647,8 @@ cudaError_t configure_linalg_attrs() {
     if ((r = cudaFuncSetAttribute(k_gemv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem))) e = r;
     if ((r = cudaFuncSetAttribute(k_symv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem))) e = r;
     if ((r = cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem))) e = r;
+    if ((r = cudaFuncSetAttribute(k_symv_ldg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLdgSmem))) e = r;
+    if ((r = cudaFuncSetAttribute(k_symv_ldg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLdgSmem))) e = r;
     return e;
 }
 
@@ -1454,6 +1676,7 @@ void preload_linalg() {
     touch_kernel(k_gemv_tiles<false, 0>); touch_kernel(k_gemv_tiles<false, 1>);
     touch_kernel(k_gemv_bulk<0>); touch_kernel(k_gemv_bulk<1>);
     touch_kernel(k_symv_bulk<0>); touch_kernel(k_symv_bulk<1>);
+    touch_kernel(k_symv_ldg<0>); touch_kernel(k_symv_ldg<1>);
     touch_kernel(k_count_asym); touch_kernel(k_spmv<0>); touch_kernel(k_spmv<1>);
     touch_kernel(k_spmv_aug<0>); touch_kernel(k_spmv_aug<1>);
 #define IPM_TOUCH_G(GG) touch_kernel(k_apply_reduce<GG, 0>); touch_kernel(k_apply_reduce<GG, 1>); \

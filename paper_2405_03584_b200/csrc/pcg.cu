@@ -1041,7 +1041,9 @@ k_spmvT(int n, const int64_t *__restrict__ ATrp, const int *__restrict__ ATcol, 
         double s = 0.0;
         const int64_t e = ATrp[i + 1];
         int64_t k = ATrp[i] + gl;       // 4 strided entries in flight per trip, folded in k order
-        if (keep) {
+        if (keep == 2) {                // experiment IPM_SPMV_VEC: column-pair loads
+            s = row_dot_pairs<G>(ATcol, ATval, t, ATrp[i], e, gl, keep_policy());
+        } else if (keep) {
             const uint64_t pol = keep_policy();
             for (; k + 3 * G < e; k += 4 * G) {
                 const int c0 = ld_keep(ATcol + k, pol), c1 = ld_keep(ATcol + k + G, pol);

@@ -36,6 +36,7 @@ ap.add_argument("--ckpt", default=None)
 ap.add_argument("--resume", default=None)
 ap.add_argument("--max-minutes", type=float, default=1e9)
 ap.add_argument("--stop-after", type=int, default=None, help="stop before QP k (resume testing)")
+ap.add_argument("--warm-shift", type=float, default=None, help="R15 theta (ipm_options.warm_shift)")
 a = ap.parse_args()
 t_wall = time.time()
 kw = {}
@@ -46,7 +47,7 @@ if a.m is not None:
 q = config("C3", 0, **kw)
 ups = sqp_sequence(q, a.K, seed=0)
 dev = torch.device("cuda", 0)
-qp = QP(device=dev, **problem_tensors(q, dev))
+qp = QP(device=dev, **problem_tensors(q, dev), **({"warm_shift": a.warm_shift} if a.warm_shift is not None else {}))
 k0 = 0
 if a.resume:
     ck = np.load(a.resume)
@@ -80,7 +81,7 @@ for k in range(k0, a.K):
     fstar = q.f_star if k == 0 else ups[k - 1].f_star
     xstar = q.x_star if k == 0 else ups[k - 1].x_star
     x = qp.solution()["x"].cpu().numpy()
-    emit({"qp": k, "mode": "cold" if a.cold else "warm", "status": st, "t_solve_s": s["t_solve_ms"] / 1e3,
+    emit({"qp": k, "mode": "cold" if a.cold else "warm", "theta": a.warm_shift, "status": st, "t_solve_s": s["t_solve_ms"] / 1e3,
           "ipm": s["ipm_iters"], "pcg": s["pcg_iters_total"], "obj": s["obj"],
           "rel_err_f_planted": abs(s["obj"] - fstar) / abs(fstar), "max_err_x_planted": float(abs(x - xstar).max())})
     if a.ckpt:
