@@ -75,7 +75,7 @@ typedef struct {
     int32_t predictor_corrector;/* 0: Alg. 1 verbatim (default); 1: Mehrotra (R18, option) */
     int32_t trace;              /* 1: record one ipm_trace_rec per IPM iteration */
     int32_t use_graph;          /* 1: PCG loop as a CUDA graph with a device-side WHILE node */
-    double warm_shift;          /* 1e-3   theta of the warm-start rule (R15) */
+    double warm_shift;          /* 0.1    theta of the warm-start rule (R15; R15) */
     int32_t gemv_kernel;        /* 0 auto: 3 when H == H^T bitwise — unsharded by a device compare at create,
                                    row-sharded by the allgathered hash certificate, and then only with an
                                    even chunk = ceil(n / nranks) — else 2.  1 LDG.128 register tiles,

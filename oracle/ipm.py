@@ -58,7 +58,7 @@ class Options:
     tau: float = 0.995
     max_iter: int = 100
     predictor_corrector: bool = False
-    warm_shift: float = 1e-3
+    warm_shift: float = 0.1          # R15 theta (R15: sweep 1e-3 .. 1 on the C4 sequence)
 
 
 @dataclasses.dataclass

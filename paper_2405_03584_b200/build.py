@@ -42,7 +42,10 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
              "hyb10": ["-DIPM_SYM_LDGW=2", "-DIPM_SYM_LDG_EVERY=10"], "hyb7": ["-DIPM_SYM_LDGW=2", "-DIPM_SYM_LDG_EVERY=7"],
              "hyb14": ["-DIPM_SYM_LDGW=2", "-DIPM_SYM_LDG_EVERY=14"], "hyb10w3": ["-DIPM_SYM_LDGW=3", "-DIPM_SYM_LDG_EVERY=10"],
              "l2p0": ["-DIPM_SYM_L2P=0"], "l2p2": ["-DIPM_SYM_L2P=2"], "nohint": ["-DIPM_SYM_NOHINT"],
-             "nohintnc": ["-DIPM_SYM_NOHINT", "-DIPM_SYM_NOCOMPUTE"], "l2p0nc": ["-DIPM_SYM_L2P=0", "-DIPM_SYM_NOCOMPUTE"]}.get(variant, [])
+             "nohintnc": ["-DIPM_SYM_NOHINT", "-DIPM_SYM_NOCOMPUTE"],
+             "ldg8d3": ["-DIPM_SYMV_LDG_DEFAULT=1"], "ldgnoring": ["-DIPM_SYMV_LDG_DEFAULT=1", "-DIPM_LDG_NORING"],
+             "ldg8d2": ["-DIPM_SYMV_LDG_DEFAULT=1", "-DIPM_LDG_DEPTH=2"],
+             "ldg16d2": ["-DIPM_SYMV_LDG_DEFAULT=1", "-DIPM_LDG_NW=16", "-DIPM_LDG_DEPTH=2"], "l2p0nc": ["-DIPM_SYM_L2P=0", "-DIPM_SYM_NOCOMPUTE"]}.get(variant, [])
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers += [os.path.join(ROOT, "include", h) for h in ("ipm.h", "sqp.h")]
     objdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))

@@ -982,7 +982,7 @@ IPM_EXPORT void ipm_options_default(ipm_options *o) {
     o->predictor_corrector = 0;
     o->trace = 0;
     o->use_graph = 1;
-    o->warm_shift = 1e-3;
+    o->warm_shift = 0.1;
     o->a_row_split = 1;
 }
 

@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <vector>
 
@@ -790,164 +791,267 @@ k_symv_bulk(const __grid_constant__ CUtensorMap tmap, const SymTile *__restrict_
 
 // ------------------------------------------- symmetric GEMV, register (LDG) streaming variant
 // Same work plan, tile semantics and ypart slots as k_symv_bulk, but H goes straight from HBM
-// into registers: 16 warps per CTA, warp w owns rows 2w and 2w + 1 of every 32-row strip, lane l
-// columns 2l + 64q + {0, 1} (q < 4) — four coalesced 16-B loads per row.  The next strip's loads
-// are issued before the current strip is reduced (two strips in flight per warp).  Row parts are
-// reduced in registers (two rows per 5-step shuffle tree); column parts accumulate per warp over
-// the tile's strips and are combined across the 16 warps through shared memory ONE strip later,
-// after the following loads are in flight (double-buffered, one named barrier per tile), in warp
-// order — deterministic.
-constexpr int kLdgWarps = 16;
-constexpr int kLdgThreads = 32 * kLdgWarps;
-constexpr size_t kLdgSmem = 2ull * kLdgWarps * kSymB * 8;
-static_assert(kLdgWarps * 2 == kSymSR, "two strip rows per warp");
+// into registers: NW warps per CTA, warp w owns rows RW w .. RW w + RW - 1 of every 32-row strip,
+// lane l columns 2l + 64q + {0, 1} (q < 4) — four coalesced 16-B loads per row.  DEPTH register
+// buffers rotate: a warp consumes strip k while strips k + 1 .. k + DEPTH - 1 are in flight.
+// Loads complete in issue order per warp, so nothing the current strip needs may be fetched through
+// the LDG queue after the look-ahead loads: p_J comes from a shared-memory ring filled by the TMA
+// unit (one slot per upcoming tile), p_I travels with its strip, the tile list is staged in shared
+// memory.  Row parts: a transpose-reduce over the lanes (RW values -> one row per lane group);
+// column parts: per-warp accumulators in shared memory, combined across the NW warps in warp order
+// at the next tile switch (one named barrier per tile) — deterministic.
+constexpr int kLdgTileCache = 2048;   // tile descriptors of the CTA's range staged in shared memory
+constexpr int kLdgPjSlots = 4;        // p_J ring (TMA bulk copies, one slot per upcoming tile)
+#ifndef IPM_LDG_NW
+#define IPM_LDG_NW 8
+#endif
+#ifndef IPM_LDG_DEPTH
+#define IPM_LDG_DEPTH 3
+#endif
+constexpr int kLdgNW = IPM_LDG_NW, kLdgRW = kSymSR / IPM_LDG_NW, kLdgDepth = IPM_LDG_DEPTH;
+static_assert(kLdgNW * kLdgRW == kSymSR, "warps x rows per warp = strip height");
+template <int NW>
+constexpr size_t ldg_smem() {
+    return 2ull * NW * kSymB * 8 + (size_t)kLdgPjSlots * kSymB * 8 + 8 * kLdgPjSlots +
+           (size_t)kLdgTileCache * sizeof(SymTile);
+}
 
 struct LdgUnit {
     int t, sidx;          // tile, strip (t > tlast: none)
 };
+// H: streamed once — no L1 allocation, L2 evict_first
+__device__ __forceinline__ double2 ld_stream2(const double *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
 
-template <int MODE>
-__global__ void __launch_bounds__(kLdgThreads, 1)
+template <int MODE, int NW, int RW, int DEPTH>
+__global__ void __launch_bounds__(NW * 32, 1)
 k_symv_ldg(const SymTile *__restrict__ tiles, const SymRange *__restrict__ ranges, const double *__restrict__ p,
            int64_t row_begin, const double *__restrict__ pdot, double *__restrict__ ypart, int ldy, int ycarry,
            double *__restrict__ zpart, int ldz, int zcarry, double *__restrict__ dpart, Scalars *sc, int cid,
            const double *__restrict__ sigb_dot, int timed, const double *__restrict__ H, int64_t ldh) {
-    extern __shared__ __align__(16) double cbuf[];        // [2][kLdgWarps][kSymB] column partials
-    __shared__ double red[kLdgWarps];
+    // dynamic smem: colacc[2][NW][kSymB] | p_J ring [kLdgPjSlots][kSymB] | its mbarriers | tiles
+    extern __shared__ __align__(16) double cbuf[];
+    __shared__ double red[NW];
     if (MODE == 1 && sc->done) return;
     if (MODE == 1 && timed) ktimer_start(&sc->kt_neg);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const SymRange rg = ranges[blockIdx.x];
     const int tlast = rg.s1 > 0 ? rg.t1 : rg.t1 - 1;
-    auto strips_end = [&](int t, const SymTile &T) { return (t == rg.t1) ? rg.s1 : (T.rows + kSymSR - 1) / kSymSR; };
-    double dacc = 0.0;
-    // loads of one strip: rows r0 = 2w, r1 = 2w + 1 of the strip, this lane's 8 columns
-    double2 h0[4], h1[4], n0[4], n1[4];
-    double pi0 = 0.0, pi1 = 0.0, npi0 = 0.0, npi1 = 0.0;
-    auto load = [&](const SymTile &T, int sidx, double2 (&a)[4], double2 (&b)[4], double &qa, double &qb) {
-        const int r = sidx * kSymSR + 2 * warp;
-        const bool ok0 = r < T.rows, ok1 = r + 1 < T.rows;
-        const double *row0 = H + (int64_t)(T.r0 + r) * ldh + T.c0;
-        const double *row1 = row0 + ldh;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int c = 2 * lane + 64 * q;
-            if (c + 1 < T.cols) {
-                a[q] = ok0 ? __ldcs(reinterpret_cast<const double2 *>(row0 + c)) : make_double2(0.0, 0.0);
-                b[q] = ok1 ? __ldcs(reinterpret_cast<const double2 *>(row1 + c)) : make_double2(0.0, 0.0);
-            } else if (c < T.cols) {                        // odd tail column
-                a[q] = make_double2(ok0 ? __ldcs(row0 + c) : 0.0, 0.0);
-                b[q] = make_double2(ok1 ? __ldcs(row1 + c) : 0.0, 0.0);
-            } else {
-                a[q] = b[q] = make_double2(0.0, 0.0);
-            }
+    double *pjring = cbuf + 2 * NW * kSymB;
+    uint64_t *pjfull = reinterpret_cast<uint64_t *>(pjring + kLdgPjSlots * kSymB);
+    SymTile *stile = reinterpret_cast<SymTile *>(pjfull + kLdgPjSlots);
+    {
+        const int nt = max(0, min(tlast - rg.t0 + 1, kLdgTileCache));
+        const int4 *src = reinterpret_cast<const int4 *>(tiles + rg.t0);
+        int4 *dst = reinterpret_cast<int4 *>(stile);
+        for (int i = threadIdx.x; i < 2 * nt; i += blockDim.x) dst[i] = src[i];
+        if (threadIdx.x == 0) {
+            for (int sl = 0; sl < kLdgPjSlots; ++sl) mbar_init(&pjfull[sl], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        const int64_t gi = row_begin + T.r0 + r;
-        qa = ok0 ? __ldg(p + gi) : 0.0;
-        qb = ok1 ? __ldg(p + gi + 1) : 0.0;
+        __syncthreads();
+    }
+    auto tile = [&](int t) -> SymTile { return (t - rg.t0 < kLdgTileCache) ? stile[t - rg.t0] : tiles[t]; };
+    uint64_t pol, pol_keep;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    auto issue_pj = [&](int t) {                         // p_J of tile t -> its ring slot (thread 0)
+        const SymTile T = tile(t);
+        const int sl = (t - rg.t0) % kLdgPjSlots;
+        const uint32_t bytes = (uint32_t)(((T.cols + 1) & ~1) * 8);
+        mbar_expect_tx(&pjfull[sl], bytes);
+        bulk_g2s(pjring + sl * kSymB, p + T.c0, bytes, &pjfull[sl], pol_keep);
     };
-    // column-part flush: colacc of this warp -> cbuf[f & 1][warp][.]; reduced one strip later
-    double2 ca[4];
+    if (threadIdx.x == 0)
+        for (int t = rg.t0; t <= min(tlast, rg.t0 + kLdgPjSlots - 2); ++t) issue_pj(t);
+    double dacc = 0.0;
+    double2 hb[DEPTH][RW][4];
+    double pb[DEPTH][RW];
+    // strip loads: rows RW w + i, this lane's 8 columns; p_I of the rows
+    auto load = [&](const SymTile &T, int sidx, double2 (&h)[RW][4], double (&pi)[RW]) {
+        const int r = sidx * kSymSR + RW * warp;
+        const double *row = H + (int64_t)(T.r0 + r) * ldh + T.c0;
+        const int64_t gi = row_begin + T.r0 + r;
+        if (r + RW <= T.rows && T.cols == kSymB) {       // full rows: unconditional 16-B loads
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ca[q] = make_double2(0.0, 0.0);
-    int nflush = 0, pend_t = -1, pend_sa = 0;
-    auto reduce_pending = [&]() {
-        asm volatile("bar.sync 1, %0;" ::"n"(kLdgThreads) : "memory");
-        const SymTile T = tiles[pend_t];
-        const double *buf = cbuf + (size_t)((nflush - 1) & 1) * kLdgWarps * kSymB;
-        if (lane < kSymB / kLdgWarps) {
-            const int c = warp * (kSymB / kLdgWarps) + lane;
-            if (c < T.cols) {
-                double colsum = 0.0;
+            for (int i = 0; i < RW; ++i)
 #pragma unroll
-                for (int w = 0; w < kLdgWarps; ++w) colsum += buf[w * kSymB + c];
-                if (T.cmode == 1) {
-                    const int slot = (pend_sa == 0) ? T.cslot : ycarry + rg.carry;
-                    ypart[(int64_t)(T.cbase + c) * ldy + slot] = colsum;
-                } else {
-                    const int slot = (pend_sa == 0) ? T.cslot : zcarry + rg.carry;
-                    zpart[(int64_t)(T.cbase + c) * ldz + slot] = colsum;
-                }
-                if (pdot) dacc = fma(__ldg(p + T.c0 + c), colsum, dacc);   // pdot: flag only (as k_symv_bulk)
+                for (int q = 0; q < 4; ++q) h[i][q] = ld_stream2(row + i * ldh + 2 * lane + 64 * q, pol);
+#pragma unroll
+            for (int i = 0; i < RW; ++i) pi[i] = __ldg(p + gi + i);
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+            const bool ok = r + i < T.rows;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int c = 2 * lane + 64 * q;
+                if (ok && c + 1 < T.cols) h[i][q] = ld_stream2(row + i * ldh + c, pol);
+                else if (ok && c < T.cols) h[i][q] = make_double2(ld_stream(row + i * ldh + c, pol), 0.0);
+                else h[i][q] = make_double2(0.0, 0.0);
             }
+            pi[i] = ok ? __ldg(p + gi + i) : 0.0;
+        }
+    };
+    int nflush = 0, pend_t = -1, pend_sa = 0;
+    // column parts of the previous off-diagonal tile: NW warps' accumulators summed in warp order
+    auto reduce_pending = [&]() {
+        const SymTile T = tile(pend_t);
+        const double *buf = cbuf + (size_t)((nflush - 1) & 1) * NW * kSymB;
+        for (int c = threadIdx.x; c < T.cols; c += NW * 32) {
+            double colsum = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) colsum += buf[w * kSymB + c];
+            if (T.cmode == 1) {
+                const int slot = (pend_sa == 0) ? T.cslot : ycarry + rg.carry;
+                ypart[(int64_t)(T.cbase + c) * ldy + slot] = colsum;
+            } else {
+                const int slot = (pend_sa == 0) ? T.cslot : zcarry + rg.carry;
+                zpart[(int64_t)(T.cbase + c) * ldz + slot] = colsum;
+            }
+            if (pdot) dacc = fma(p[T.c0 + c], colsum, dacc);   // pdot: flag only (as k_symv_bulk)
         }
         pend_t = -1;
     };
-    LdgUnit cur{rg.t0, rg.s0};
-    if (cur.t <= tlast) {
-        const SymTile T = tiles[cur.t];
-        load(T, cur.sidx, h0, h1, pi0, pi1);
-    }
-    while (cur.t <= tlast) {
-        const SymTile T = tiles[cur.t];
+    auto advance = [&](LdgUnit u) -> LdgUnit {
+        const SymTile T = tile(u.t);
+        const int se = (u.t == rg.t1) ? rg.s1 : (T.rows + kSymSR - 1) / kSymSR;
+        LdgUnit v{u.t, u.sidx + 1};
+        if (v.sidx >= se) { v.t = u.t + 1; v.sidx = 0; }
+        return v;
+    };
+    // look-ahead queue of units: uq[d] = strip k + d (sentinel t = tlast + 1 past the range);
+    // uq[0 .. DEPTH - 2] are loaded, uq[DEPTH - 1] is loaded by the step that consumes uq[0]
+    LdgUnit uq[DEPTH];
+    uq[0] = LdgUnit{rg.t0, rg.s0};
+#pragma unroll
+    for (int d = 1; d < DEPTH; ++d) uq[d] = (uq[d - 1].t <= tlast) ? advance(uq[d - 1]) : LdgUnit{tlast + 1, 0};
+#pragma unroll
+    for (int d = 0; d < DEPTH - 1; ++d)
+        if (uq[d].t <= tlast) load(tile(uq[d].t), uq[d].sidx, hb[d], pb[d]);
+    auto step = [&](auto XI) {
+        constexpr int X = decltype(XI)::value;              // buffer of the current strip
+        constexpr int Y = (X + DEPTH - 1) % DEPTH;          // buffer for the strip DEPTH - 1 ahead
+        const LdgUnit cur = uq[0];
+        const SymTile T = tile(cur.t);
         const int sa = (cur.t == rg.t0) ? rg.s0 : 0;
-        const int sb = strips_end(cur.t, T);
-        LdgUnit nx{cur.t, cur.sidx + 1};
-        if (nx.sidx >= sb) { nx.t = cur.t + 1; nx.sidx = 0; }
-        if (nx.t <= tlast) {
-            const SymTile TN = tiles[nx.t];
-            load(TN, nx.sidx, n0, n1, npi0, npi1);
+        const bool first = (cur.sidx == sa);
+        if (uq[DEPTH - 1].t <= tlast) load(tile(uq[DEPTH - 1].t), uq[DEPTH - 1].sidx, hb[Y], pb[Y]);
+        const int sl = (cur.t - rg.t0) % kLdgPjSlots;
+        if (first) {
+            if (cur.t > rg.t0) {
+                // every warp is done with tile cur.t - 1: combine its column parts, refill its slot
+                asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+                if (pend_t >= 0) reduce_pending();
+            }
+            if (threadIdx.x == 0 && cur.t + kLdgPjSlots - 1 <= tlast) issue_pj(cur.t + kLdgPjSlots - 1);
+            mbar_wait(&pjfull[sl], (uint32_t)(((cur.t - rg.t0) / kLdgPjSlots) & 1));
         }
-        if (pend_t >= 0) reduce_pending();               // the next strip's loads are in flight
-        // row parts of rows 2w, 2w + 1 against p_J (L1-resident after the first warp)
-        double s0 = 0.0, s1 = 0.0;
-        double2 pj[4];
+        const double2 *pjv = reinterpret_cast<const double2 *>(pjring + sl * kSymB);
+        double s[RW];
+#pragma unroll
+        for (int i = 0; i < RW; ++i) s[i] = 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int c = 2 * lane + 64 * q;
-            pj[q] = (c + 1 < T.cols) ? __ldg(reinterpret_cast<const double2 *>(p + T.c0 + c))
-                                     : make_double2(c < T.cols ? __ldg(p + T.c0 + c) : 0.0, 0.0);
-        }
+#ifdef IPM_LDG_NORING
+            double2 pj = (c + 1 < T.cols) ? __ldg(reinterpret_cast<const double2 *>(p + T.c0 + c))
+                                          : make_double2(c < T.cols ? __ldg(p + T.c0 + c) : 0.0, 0.0);
+#else
+            double2 pj = pjv[lane + 32 * q];
+#endif
+            if (c + 1 >= T.cols) pj = make_double2(c < T.cols ? pj.x : 0.0, 0.0);   // past the tile
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            s0 = fma(h0[q].x, pj[q].x, s0);
-            s0 = fma(h0[q].y, pj[q].y, s0);
-            s1 = fma(h1[q].x, pj[q].x, s1);
-            s1 = fma(h1[q].y, pj[q].y, s1);
+            for (int i = 0; i < RW; ++i) {
+                s[i] = fma(hb[X][i][q].x, pj.x, s[i]);
+                s[i] = fma(hb[X][i][q].y, pj.y, s[i]);
+            }
         }
-        const bool hi = lane & 16;
-        double v = (hi ? s1 : s0) + __shfl_xor_sync(0xffffffffu, hi ? s0 : s1, 16);
+        // transpose-reduce: halve the live rows per xor stage, then a plain tree
+        int off = 16, nr = RW, row_of = 0;
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        const int r = cur.sidx * kSymSR + 2 * warp + (hi ? 1 : 0);
-        if ((lane & 15) == 0 && r < T.rows) {
+        for (int st = 0; st < 5; ++st) {
+            const bool hi = lane & off;
+            if (nr > 1) {
+#pragma unroll
+                for (int i = 0; i < RW / 2; ++i) {
+                    if (i < nr / 2) {
+                        const double send = hi ? s[i] : s[i + nr / 2];
+                        const double keep = hi ? s[i + nr / 2] : s[i];
+                        s[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                    }
+                }
+                row_of = 2 * row_of + (hi ? 1 : 0);
+                nr /= 2;
+            } else {
+                s[0] += __shfl_xor_sync(0xffffffffu, s[0], off);
+            }
+            off >>= 1;
+        }
+        // lane l now holds the sum of strip row RW w + row_of (row_of from its top log2(RW) bits)
+        constexpr int kGroup = 32 / RW;
+        const int r = cur.sidx * kSymSR + RW * warp + row_of;
+        if ((lane & (kGroup - 1)) == 0 && r < T.rows) {
+            const double v = s[0];
             ypart[(int64_t)(T.r0 + r) * ldy + T.rslot] = v;
             if (pdot) {
-                const double pr = hi ? pi1 : pi0;
+                double pr = pb[X][0];
+#pragma unroll
+                for (int i = 1; i < RW; ++i) if (row_of == i) pr = pb[X][i];
                 dacc = fma(pr, v, dacc);
                 if (sigb_dot && T.cmode == 0) dacc = fma(sigb_dot[T.r0 + r] * pr, pr, dacc);
             }
         }
-        if (T.cmode != 0) {                              // column parts: rows 2w then 2w + 1
+        if (T.cmode != 0) {                              // column parts, rows in order
+            double2 *acc = reinterpret_cast<double2 *>(cbuf + (size_t)(nflush & 1) * NW * kSymB + warp * kSymB);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                ca[q].x = fma(h0[q].x, pi0, ca[q].x);
-                ca[q].y = fma(h0[q].y, pi0, ca[q].y);
-                ca[q].x = fma(h1[q].x, pi1, ca[q].x);
-                ca[q].y = fma(h1[q].y, pi1, ca[q].y);
-            }
-            if (nx.t != cur.t) {                         // last strip of the tile in this range
-                double *buf = cbuf + (size_t)(nflush & 1) * kLdgWarps * kSymB + warp * kSymB;
+                double2 c2 = first ? make_double2(0.0, 0.0) : acc[lane + 32 * q];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    reinterpret_cast<double2 *>(buf)[lane + 32 * q] = ca[q];
-                    ca[q] = make_double2(0.0, 0.0);
+                for (int i = 0; i < RW; ++i) {
+                    c2.x = fma(hb[X][i][q].x, pb[X][i], c2.x);
+                    c2.y = fma(hb[X][i][q].y, pb[X][i], c2.y);
                 }
+                acc[lane + 32 * q] = c2;
+            }
+            if (uq[1].t != cur.t) {                      // last strip of the tile in this range
                 ++nflush;
                 pend_t = cur.t;
                 pend_sa = sa;
             }
         }
-        cur = nx;
+        const LdgUnit nl = (uq[DEPTH - 1].t <= tlast) ? advance(uq[DEPTH - 1]) : LdgUnit{tlast + 1, 0};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            h0[q] = n0[q];
-            h1[q] = n1[q];
+        for (int d = 0; d < DEPTH - 1; ++d) uq[d] = uq[d + 1];
+        uq[DEPTH - 1] = nl;
+    };
+    while (uq[0].t <= tlast) {
+        step(std::integral_constant<int, 0>{});
+        if (uq[0].t > tlast) break;
+        step(std::integral_constant<int, 1>{});
+        if (DEPTH > 2) {
+            if (uq[0].t > tlast) break;
+            step(std::integral_constant<int, (DEPTH > 2 ? 2 : 0)>{});
         }
-        pi0 = npi0;
-        pi1 = npi1;
+        if (DEPTH > 3) {
+            if (uq[0].t > tlast) break;
+            step(std::integral_constant<int, (DEPTH > 3 ? 3 : 0)>{});
+        }
     }
-    if (pend_t >= 0) reduce_pending();
+    if (rg.t0 <= tlast) {
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+        if (pend_t >= 0) reduce_pending();
+    }
     if (pdot == nullptr) return;
     const double bs = block_sum(dacc, red);
     if (threadIdx.x == 0) dpart[blockIdx.x] = bs;
@@ -966,7 +1070,10 @@ static int symv_ldg_enabled() {
     static int e = -1;
     if (e < 0) {
         const char *v = getenv("IPM_SYMV_LDG");         // experiment switch: 1 = register-streaming SYMV
-        e = v ? atoi(v) : 0;
+#ifndef IPM_SYMV_LDG_DEFAULT
+#define IPM_SYMV_LDG_DEFAULT 0
+#endif
+        e = v ? atoi(v) : IPM_SYMV_LDG_DEFAULT;
     }
     return e;
 }
@@ -989,11 +1096,11 @@ void launch_symv_bulk(const Prob &P, const double *v, const double *vdot, double
 #endif
     if (symv_ldg_enabled() && (P.ldh % 2) == 0) {
         if (mode == 1)
-            k_symv_ldg<1><<<grid, kLdgThreads, kLdgSmem, st>>>(P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
+            k_symv_ldg<1, kLdgNW, kLdgRW, kLdgDepth><<<grid, kLdgNW * 32, ldg_smem<kLdgNW>(), st>>>(P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
                                                                P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
                                                                dpart, sc, cid, sigb_dot, P.ktimer, P.H, P.ldh);
         else
-            k_symv_ldg<0><<<grid, kLdgThreads, kLdgSmem, st>>>(P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
+            k_symv_ldg<0, kLdgNW, kLdgRW, kLdgDepth><<<grid, kLdgNW * 32, ldg_smem<kLdgNW>(), st>>>(P.sym_tiles, P.sym_ranges, v, P.row_begin, vdot, ypart,
                                                                P.ncb, P.sym_ycarry, P.sym_z, P.sym_ldz, P.sym_zcarry,
                                                                dpart, sc, cid, sigb_dot, P.ktimer, P.H, P.ldh);
         return;
@@ -1647,8 +1754,12 @@ cudaError_t configure_linalg_attrs() {
     if ((r = cudaFuncSetAttribute(k_gemv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem))) e = r;
     if ((r = cudaFuncSetAttribute(k_symv_bulk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem))) e = r;
     if ((r = cudaFuncSetAttribute(k_symv_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem))) e = r;
-    if ((r = cudaFuncSetAttribute(k_symv_ldg<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLdgSmem))) e = r;
-    if ((r = cudaFuncSetAttribute(k_symv_ldg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLdgSmem))) e = r;
+    if ((r = cudaFuncSetAttribute(k_symv_ldg<0, kLdgNW, kLdgRW, kLdgDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ldg_smem<kLdgNW>())))
+        e = r;
+    if ((r = cudaFuncSetAttribute(k_symv_ldg<1, kLdgNW, kLdgRW, kLdgDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ldg_smem<kLdgNW>())))
+        e = r;
     return e;
 }
 
@@ -1676,7 +1787,7 @@ void preload_linalg() {
     touch_kernel(k_gemv_tiles<false, 0>); touch_kernel(k_gemv_tiles<false, 1>);
     touch_kernel(k_gemv_bulk<0>); touch_kernel(k_gemv_bulk<1>);
     touch_kernel(k_symv_bulk<0>); touch_kernel(k_symv_bulk<1>);
-    touch_kernel(k_symv_ldg<0>); touch_kernel(k_symv_ldg<1>);
+    touch_kernel(k_symv_ldg<0, kLdgNW, kLdgRW, kLdgDepth>); touch_kernel(k_symv_ldg<1, kLdgNW, kLdgRW, kLdgDepth>);
     touch_kernel(k_count_asym); touch_kernel(k_spmv<0>); touch_kernel(k_spmv<1>);
     touch_kernel(k_spmv_aug<0>); touch_kernel(k_spmv_aug<1>);
 #define IPM_TOUCH_G(GG) touch_kernel(k_apply_reduce<GG, 0>); touch_kernel(k_apply_reduce<GG, 1>); \

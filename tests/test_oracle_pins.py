@@ -293,7 +293,7 @@ def test_warm_start_point_hand_values():
     p = Problem(H=np.eye(3), g=np.zeros(3), A=np.array([[1.0, 1.0, 0.0]]), l=np.array([0.5]),
                 u=np.array([np.inf]), xl=np.array([0.0, 0.0, -np.inf]), xu=np.array([1.0, 0.002, 3.0]))
     lam = {"lA": np.array([0.25]), "uA": np.zeros(0), "lx": np.array([2.0, 0.0]), "ux": np.array([0.0, 0.5, 0.0])}
-    w = warm_start_point(p, np.array([0.0, 5.0, 3.5]), lam, Options())
+    w = warm_start_point(p, np.array([0.0, 5.0, 3.5]), lam, Options(warm_shift=1e-3))
     np.testing.assert_allclose(w.x, [1e-3, 1.5e-3, 2.999], rtol=0, atol=1e-15)
     np.testing.assert_allclose(w.s["lA"], [1e-3], rtol=0, atol=1e-15)
     np.testing.assert_allclose(w.s["lx"], [1e-3, 1.5e-3], rtol=0, atol=1e-15)
