@@ -730,20 +730,25 @@ ipm_status pcg_solve(ipm_ctx *ctx, double rtol, PcgOut &out, int64_t fixed = 0, 
     return IPM_OK;
 }
 
-// Hx (GEMV tiles) + Ax (SpMV), then the residual kernels at the given mu.
-ipm_status residuals(ipm_ctx *ctx, double mu) {
+// Hx (GEMV tiles) + Ax (SpMV), then the residual kernels at the given mu.  reuse: x has not
+// moved since the last call (its H x tile partials and A x are still in ypart / Ax) — only the
+// residual kernels run (the final report at a new mu).
+ipm_status residuals(ipm_ctx *ctx, double mu, bool reuse = false) {
     const Prob &P = ctx->P;
     const Vecs &V = ctx->V;
-    const double *xf = nullptr;
-    TRY(gather(ctx, V.x, &xf));
-    launch_gemv(P, xf, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
-    TRY(sym_exchange(ctx));
-    DSYNC("gemv Hx");
-    launch_spmv(P, xf, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
-    DSYNC("spmv Ax");
+    if (!reuse) {
+        const double *xf = nullptr;
+        TRY(gather(ctx, V.x, &xf));
+        launch_gemv(P, xf, nullptr, V.ypart, ctx->ncb, V.part[4], ctx->sc, ctx->gemv_grid, 0, C_GEMV, ctx->st);
+        TRY(sym_exchange(ctx));
+        DSYNC("gemv Hx");
+        launch_spmv(P, xf, nullptr, V.Ax, nullptr, ctx->sc, 0, 0, ctx->st);
+        DSYNC("spmv Ax");
+        ctx->launches += 1 + (P.m > 0 ? 1 : 0);
+    }
     launch_residuals(P, V, ctx->G, ctx->sc, mu, ctx->st);
     DSYNC("residual kernels");
-    ctx->launches += 2 + 2 * (P.m > 0 ? 1 : 0);
+    ctx->launches += 1 + (P.m > 0 ? 1 : 0);
     CKL();
     TRY(xcombine(ctx, X_RESID));
     return IPM_OK;
@@ -913,8 +918,9 @@ ipm_status solve_impl(ipm_ctx *ctx) {
         }
     }
     ctx->mu = mu;
-    // final residuals at the final mu (r_c with the current mu) for reporting
-    TRY(residuals(ctx, mu));
+    // final residuals at the final mu (r_c with the current mu) for reporting; x is unchanged
+    // since the last residuals (same H x, A x)
+    TRY(residuals(ctx, mu, true));
     TRY(sync_scalars(ctx));
     CK(cudaEventRecord(ctx->ev[1], ctx->st));
     CK(cudaEventSynchronize(ctx->ev[1]));
