@@ -16,7 +16,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
 SOURCES = ["linalg.cu", "compact.cu", "pcg.cu", "ipmops.cu", "shard.cu", "peer.cu", "comm.cu", "ipm_api.cu",
-           "sqp.cu"]
+           "sqp.cu", "tiny.cu"]
 
 
 def _stale(out: str, deps) -> bool:

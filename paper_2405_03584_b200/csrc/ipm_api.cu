@@ -185,6 +185,9 @@ struct ipm_ctx {
     bool cg = false;             // Chronopoulos-Gear single-reduction PCG (sharded, opt.pcg_single_reduction)
     ipm::PeerArgs peer{};
     std::vector<void *> ipc_opened;
+    // one-warp whole-IPM path (tiny.cu): mapped pinned host buffer for its result and trace
+    void *tiny_host = nullptr;
+    size_t tiny_cap = 0;
 };
 
 namespace {
@@ -807,6 +810,78 @@ ipm_status start_point(ipm_ctx *ctx) {
     return IPM_OK;
 }
 
+// n, m <= kWarpMaxN, plain Algorithm 1 (no predictor-corrector, no PCG warm start), condensed
+// system, explicit H, one GPU: the whole loop in one warp (tiny.cu).  IPM_TINY=0 disables.
+static bool tiny_path(const ipm_ctx *ctx) {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("IPM_TINY");
+        env = e ? atoi(e) : 1;
+    }
+    const Prob &P = ctx->P;
+    return env && !ctx->sharded && !P.aug && !P.hess_compact && tiny_eligible(P.n, P.m) &&
+           !ctx->opt.predictor_corrector && !ctx->opt.pcg_warm_start && ctx->opt.use_graph;
+}
+
+// Algorithm 1 after the start point, in one launch; stats, trace and status from its result.
+ipm_status solve_tiny(ipm_ctx *ctx) {
+    const ipm_options &o = ctx->opt;
+    const Prob &P = ctx->P;
+    Vecs &V = ctx->V;
+    ipm_stats &S = ctx->stats;
+    const size_t need = sizeof(TinyOut) + sizeof(ipm_trace_rec) * (size_t)std::max(1, o.max_ipm_iter);
+    if (ctx->tiny_cap < need) {
+        if (ctx->tiny_host) CK(cudaFreeHost(ctx->tiny_host));
+        ctx->tiny_host = nullptr;
+        ctx->tiny_cap = 0;
+        CK(cudaHostAlloc(&ctx->tiny_host, need, cudaHostAllocMapped));
+        ctx->tiny_cap = need;
+    }
+    TinyOut *out = reinterpret_cast<TinyOut *>(ctx->tiny_host);
+    ipm_trace_rec *tr = reinterpret_cast<ipm_trace_rec *>(out + 1);
+    TinyArgs a{};
+    a.n = P.n; a.m = P.m; a.H = P.H; a.ldh = P.ldh; a.Arp = P.Arp; a.Acol = P.Acol; a.Aval = P.Aval;
+    a.g = P.g; a.l = P.l; a.u = P.u; a.xl = P.xl; a.xu = P.xu;
+    a.x = V.x; a.s_lA = V.s_lA; a.s_uA = V.s_uA; a.lam_lA = V.lam_lA; a.lam_uA = V.lam_uA;
+    a.s_lx = V.s_lx; a.s_ux = V.s_ux; a.lam_lx = V.lam_lx; a.lam_ux = V.lam_ux; a.dx = V.dx; a.Hx = V.Hx; a.Ax = V.Ax;
+    a.mu0 = ctx->mu; a.mu_tol = o.mu_tol; a.mu_div = o.mu_divisor; a.tau = o.tau;
+    a.rtol_floor = o.pcg_rtol_floor; a.rtol_max = o.pcg_rtol_max; a.rtol_fac = o.pcg_rtol_mu_factor; a.atol = o.pcg_atol;
+    a.schedule = o.pcg_schedule; a.max_ipm = o.max_ipm_iter; a.trace = o.trace ? 1 : 0; a.pcg_maxit = o.pcg_max_iter;
+    a.trace_buf = tr;
+    a.out = out;
+    a.sc = ctx->sc;
+    out->status = -1;
+    launch_ipm_tiny(a, ctx->st);
+    ctx->launches += 1;
+    CKL();
+    TRY(sync_scalars(ctx));
+    CK(cudaEventRecord(ctx->ev[1], ctx->st));
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+    ctx->have_dx = true;
+    ctx->mu = out->mu;
+    S.ipm_iters = out->ipm_iters;
+    S.pcg_iters_total = out->pcg_total;
+    S.pcg_iters_max = out->pcg_max;
+    S.pcg_stalls = out->stalls;
+    S.pcg_restarts = out->restarts;
+    S.mu_final = out->mu;
+    S.kkt_inf = kkt_inf(*ctx->hsc);
+    S.obj = ctx->hsc->obj;
+    S.t_solve_ms = ms;
+    S.t_pcg_ms = (float)(out->t_pcg_ns * 1e-6);
+    if (o.trace)
+        for (int i = 0; i < out->ntrace; ++i) ctx->trace.push_back(tr[i]);
+    const ipm_status st = (ipm_status)out->status;
+    S.status = st;
+    if (st == IPM_ERR_PCG_BREAKDOWN)
+        return fail(ctx, st, "PCG breakdown at IPM iteration %d (one-warp path)", out->ipm_iters);
+    if (st == IPM_ERR_NONFINITE)
+        return fail(ctx, st, "non-finite residual or step at IPM iteration %d (one-warp path)", out->ipm_iters);
+    return st;
+}
+
 ipm_status solve_impl(ipm_ctx *ctx) {
     const ipm_options &o = ctx->opt;
     ctx->trace.clear();
@@ -819,6 +894,7 @@ ipm_status solve_impl(ipm_ctx *ctx) {
     DSYNC("event");
     TRY(start_point(ctx));
     ctx->have_iterate = true;
+    if (tiny_path(ctx)) return solve_tiny(ctx);
     TRY(residuals(ctx, ctx->mu));
     TRY(sync_scalars(ctx));
     // a starting iterate with Inf/NaN entries (ipm_set_iterate) cannot produce a direction
@@ -1319,6 +1395,7 @@ static ipm_status create_impl(ipm_ctx *ctx, const ipm_problem *p, void *workspac
         {   // function attributes are per device: set them for this context's device on every create
             CK(configure_linalg_attrs());
             CK(configure_pcg_attrs());
+            CK(configure_tiny_attrs());
             const char *ce = getenv("IPM_CARVEOUT");
             if (!(ce && atoi(ce) == 0)) {
                 configure_linalg_carveout();
@@ -1725,6 +1802,7 @@ IPM_EXPORT void ipm_destroy(ipm_ctx *ctx) {
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->hsc) cudaFreeHost(ctx->hsc);
+    if (ctx->tiny_host) cudaFreeHost(ctx->tiny_host);
     for (void *p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     delete ctx->comm;
     delete ctx;

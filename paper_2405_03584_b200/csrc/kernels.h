@@ -108,6 +108,7 @@ void preload_ipmops();
 void preload_shard();
 void preload_peer();
 void preload_compact();
+void preload_tiny();
 inline void preload_all_kernels() {
     preload_linalg();
     preload_pcg();
@@ -115,7 +116,36 @@ inline void preload_all_kernels() {
     preload_shard();
     preload_peer();
     preload_compact();
+    preload_tiny();
 }
+
+// tiny.cu — the whole Algorithm 1 loop in one warp (n, m <= kWarpMaxN)
+struct TinyOut {
+    int32_t status, ipm_iters, pcg_max, stalls, restarts, ntrace;
+    int64_t pcg_total, pcg_it_last;
+    double mu;
+    unsigned long long t_pcg_ns;
+};
+struct TinyArgs {
+    int n, m;
+    const double *H;
+    int64_t ldh;
+    const int64_t *Arp;
+    const int *Acol;
+    const double *Aval;
+    const double *g, *l, *u, *xl, *xu;
+    double *x, *s_lA, *s_uA, *lam_lA, *lam_uA, *s_lx, *s_ux, *lam_lx, *lam_ux, *dx, *Hx, *Ax;
+    double mu0, mu_tol, mu_div, tau, rtol_floor, rtol_max, rtol_fac, atol;
+    int schedule, max_ipm, trace;
+    int64_t pcg_maxit;
+    void *trace_buf;                       // ipm_trace_rec[max_ipm] (device)
+    TinyOut *out;
+    Scalars *sc;
+};
+bool tiny_eligible(int n, int m);
+size_t tiny_smem_bytes();
+void launch_ipm_tiny(const TinyArgs &a, cudaStream_t st);
+cudaError_t configure_tiny_attrs();
 void configure_pcg_carveout();
 // NEXT-2 doubly augmented operator: t = 2 sig_c o (A px) + pl - pu, yl = A px + D_l pl,
 // yu = -A px + D_u pu (masked); mode 1 (PCG): done check + S_c = a.t + pl.yl + pu.yu

@@ -338,3 +338,39 @@ def test_symmetric_gemv_interleaved_order(n, m, monkeypatch):
     assert np.linalg.norm(y - yref) <= 1e-12 * np.linalg.norm(yref)
     sb, sc, v = _rand_sigmas(q, 5, dyadic=True)
     assert np.array_equal(qp.op_apply(sb, sc, v).cpu().numpy(), okkt.condensed_apply(q.H, q.A_dense(), sb, sc, v))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_one_warp_ipm_matches_multi_kernel_path(seed):
+    """n, m <= 64: the whole Algorithm 1 loop runs in one warp (tiny.cu).  It follows the
+    multi-kernel path's formulas and stopping rules, so against that path (use_graph=0 keeps the
+    tiny problem on it) the IPM count, the trace, x and the objective agree to rounding; the
+    oracle comparison of the same problems is test_ipm_C1_matches_oracle."""
+    q = config("C1", seed)
+    a = _qp(q, trace=1)                 # one-warp path
+    b = _qp(q, trace=1, use_graph=0)    # per-kernel host loop
+    assert a.solve() == "ok" and b.solve() == "ok"
+    sa, sb_ = a.stats(), b.stats()
+    assert sa["ipm_iters"] == sb_["ipm_iters"]
+    assert abs(sa["pcg_iters_total"] - sb_["pcg_iters_total"]) <= 0.2 * sb_["pcg_iters_total"]
+    assert sa["t_pcg_ms"] > 0.0 and sa["t_pcg_ms"] <= sa["t_solve_ms"]
+    xa, xb = a.solution()["x"].cpu().numpy(), b.solution()["x"].cpu().numpy()
+    assert np.max(np.abs(xa - xb)) <= 1e-9 * max(1.0, np.max(np.abs(xb)))
+    assert abs(sa["obj"] - sb_["obj"]) <= 1e-12 * abs(sb_["obj"])
+    ta, tb = a.trace(), b.trace()
+    assert len(ta) == len(tb) == sa["ipm_iters"]
+    for ra, rb in zip(ta, tb):
+        assert ra["it"] == rb["it"] and ra["mu"] == rb["mu"]
+        assert abs(ra["obj"] - rb["obj"]) <= 1e-9 * max(1.0, abs(rb["obj"]))
+    # a second solve from the stored state (warm start is the multi-kernel path's) still works
+    a.warm_start()
+    assert a.solve() == "ok"
+
+
+def test_one_warp_ipm_iteration_limit():
+    """max_ipm_iter reached on the one-warp path: IPM_NOT_CONVERGED with the iterate kept."""
+    q = config("C1", 0)
+    a = _qp(q, max_ipm_iter=3, trace=1)
+    assert a.solve(raise_on_error=False) == "not_converged"
+    s = a.stats()
+    assert s["ipm_iters"] == 3 and len(a.trace()) == 3 and np.all(np.isfinite(a.solution()["x"].cpu().numpy()))
