@@ -33,6 +33,21 @@ constexpr int kLd = kT + 1;            // odd smem row stride: conflict-free row
 constexpr int kNV = 25, kMV = 21;      // n- and m-space vectors in shared memory
 }  // namespace
 
+// sum_k u[k * su] v[k * sv], k < len, four FMA chains combined in a fixed order (latency-bound
+// walks over shared memory otherwise dominate the non-PCG part of an IPM iteration)
+__device__ __forceinline__ double dot4(const double *u, int su, const double *v, int sv, int len) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int k = 0;
+    for (; k + 3 < len; k += 4) {
+        a0 = fma(u[k * su], v[k * sv], a0);
+        a1 = fma(u[(k + 1) * su], v[(k + 1) * sv], a1);
+        a2 = fma(u[(k + 2) * su], v[(k + 2) * sv], a2);
+        a3 = fma(u[(k + 3) * su], v[(k + 3) * sv], a3);
+    }
+    for (; k < len; ++k) a0 = fma(u[k * su], v[k * sv], a0);
+    return (a0 + a1) + (a2 + a3);
+}
+
 size_t tiny_smem_bytes() { return 8 * ((size_t)3 * kT * kLd + (size_t)(kNV + kMV) * kT); }
 
 bool tiny_eligible(int n, int m) { return n >= 1 && n <= kT && m >= 0 && m <= kT; }
@@ -75,11 +90,7 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
     int nonfinite = 0;
     // ---- residuals at mu (ipmops.cu k_resid_m / k_resid_n)
     auto residuals = [&](double mu) {
-        for (int i = l; i < m; i += 32) {
-            double s = 0.0;
-            for (int j = 0; j < n; ++j) s = fma(sA[i * kLd + j], x[j], s);
-            Ax[i] = s;
-        }
+        for (int i = l; i < m; i += 32) Ax[i] = dot4(sA + i * kLd, 1, x, 1, n);
         double prim = 0.0, comp = 0.0, lsm = 0.0, rhm = 0.0, ob = 0.0;
         int bad = 0;
         for (int i = l; i < m; i += 32) {
@@ -107,9 +118,7 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
         }
         __syncwarp();
         for (int j = l; j < n; j += 32) {
-            double hs = 0.0, at = 0.0;
-            for (int k = 0; k < n; ++k) hs = fma(sH[j * kLd + k], x[k], hs);
-            for (int i = 0; i < m; ++i) at = fma(sA[i * kLd + j], lamd[i], at);
+            const double hs = dot4(sH + j * kLd, 1, x, 1, n), at = dot4(sA + j, kLd, lamd, 1, m);
             const double xj = x[j];
             hx[j] = hs;
             const double r = hs + g[j] - at - llx[j] + lux[j];
@@ -160,11 +169,15 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
         }
         __syncwarp();
         for (int j = l; j < n; j += 32) {
-            double s = 0.0;
-            for (int i = 0; i < m; ++i) {
-                const double aij = sA[i * kLd + j];
-                s = fma(aij * aij, sigc[i], s);
+            double s0 = 0.0, s1 = 0.0;
+            int i = 0;
+            for (; i + 1 < m; i += 2) {
+                const double a0 = sA[i * kLd + j], a1 = sA[(i + 1) * kLd + j];
+                s0 = fma(a0 * a0, sigc[i], s0);
+                s1 = fma(a1 * a1, sigc[i + 1], s1);
             }
+            if (i < m) s0 = fma(sA[i * kLd + j] * sA[i * kLd + j], sigc[i], s0);
+            const double s = s0 + s1;
             double sb = 0.0;
             if (has(xl[j])) sb += llx[j] / slx[j];
             if (has(xu[j])) sb += lux[j] / sux[j];
@@ -194,8 +207,7 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
         }
         __syncwarp();
         for (int j = l; j < n; j += 32) {
-            double at = 0.0;
-            for (int i = 0; i < m; ++i) at = fma(sA[i * kLd + j], wv[i], at);
+            const double at = dot4(sA + j, kLd, wv, 1, m);
             double r1 = -rH[j], ca = 0.0, cb = 0.0;
             if (has(xl[j])) {
                 ca = llx[j] * slx[j] - mu;
@@ -209,37 +221,58 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
             rcux[j] = cb;
             rhs[j] = fma(1.0, at, r1);
         }
-        // K = (H + sum_i sigma_i (A_ij A_ik)) + delta_jk sigma_b,j — k_form_K's association
+        // K = (H + sum_r sigma_r (A_rj A_rk)) + delta_jk sigma_b,j over the rows r with A_rj != 0 in
+        // ascending r — k_form_K's terms and association, so the same bits.  Stored TRANSPOSED
+        // (sK[k * 64 + j] = K_jk; lane j owns column j, so every walk is lane-consecutive) and
+        // accumulated in place one row of A at a time (independent FMAs across k).
         for (int j = l; j < n; j += 32)
-            for (int k = 0; k < n; ++k) {
-                double acc = 0.0;
-                for (int i = 0; i < m; ++i) acc = fma(sigc[i], sA[i * kLd + j] * sA[i * kLd + k], acc);
-                sK[j * kLd + k] = (sH[j * kLd + k] + acc) + (j == k ? sigb[j] : 0.0);
+            for (int k = 0; k < n; ++k) sK[k * kT + j] = 0.0;
+        for (int r = 0; r < m; ++r) {
+            const double sr = sigc[r];
+            const double *ar = sA + r * kLd;
+            for (int j = l; j < n; j += 32) {
+                const double a = ar[j];
+                if (a == 0.0) continue;
+#pragma unroll 4
+                for (int k = 0; k < n; ++k) sK[k * kT + j] = fma(sr, a * ar[k], sK[k * kT + j]);
             }
-        __syncwarp();
-        // PCG from x0 = 0 (k_pcg_init), stopping rule S:225, restarts on the true residual
-        auto kmul = [&](const double *u, int j) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int k = 0;
-            for (; k + 3 < n; k += 4) {
-                a0 = fma(sK[j * kLd + k], u[k], a0);
-                a1 = fma(sK[j * kLd + k + 1], u[k + 1], a1);
-                a2 = fma(sK[j * kLd + k + 2], u[k + 2], a2);
-                a3 = fma(sK[j * kLd + k + 3], u[k + 3], a3);
-            }
-            for (; k < n; ++k) a0 = fma(sK[j * kLd + k], u[k], a0);
-            return (a0 + a1) + (a2 + a3);
-        };
-        double rz = 0.0, rr0 = 0.0;
-        for (int j = l; j < n; j += 32) {
-            const double r = rhs[j], z = minv[j] * r;
-            dx[j] = 0.0;
-            rv[j] = r;
-            zv[j] = z;
-            rz = fma(r, z, rz);
-            rr0 = fma(r, r, rr0);
         }
-        double rho = warp_sum(rz), rr = warp_sum(rr0), rho_old = rho;
+        for (int j = l; j < n; j += 32)
+            for (int k = 0; k < n; ++k)
+                sK[k * kT + j] = (sH[j * kLd + k] + sK[k * kT + j]) + (j == k ? sigb[j] : 0.0);
+        // PCG from x0 = 0 (k_pcg_init), stopping rule S:225, restarts on the true residual — the
+        // register-resident loop of k_pcg_warp: lane l owns rows l and l + 32, u broadcast from sp
+        const int i0 = l, i1 = l + 32;
+        const bool h0 = i0 < n, h1 = i1 < n;
+        auto kmul = [&](const double *u, double &o0, double &o1) {   // (K u) rows i0, i1 (k_pcg_warp's)
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+            const int n4 = n & ~3;
+            int k = 0;
+#pragma unroll 4
+            for (; k < n4; k += 4) {
+                const double2 ua = *reinterpret_cast<const double2 *>(u + k);
+                const double2 ub = *reinterpret_cast<const double2 *>(u + k + 2);
+                const double *kr = sK + k * kT;
+                a0 = fma(kr[i0], ua.x, a0);
+                c0 = fma(kr[i1], ua.x, c0);
+                a1 = fma(kr[kT + i0], ua.y, a1);
+                c1 = fma(kr[kT + i1], ua.y, c1);
+                a2 = fma(kr[2 * kT + i0], ub.x, a2);
+                c2 = fma(kr[2 * kT + i1], ub.x, c2);
+                a3 = fma(kr[3 * kT + i0], ub.y, a3);
+                c3 = fma(kr[3 * kT + i1], ub.y, c3);
+            }
+            for (; k < n; ++k) {
+                a0 = fma(sK[k * kT + i0], u[k], a0);
+                c0 = fma(sK[k * kT + i1], u[k], c0);
+            }
+            o0 = h0 ? (a0 + a1) + (a2 + a3) : 0.0;
+            o1 = h1 ? (c0 + c1) + (c2 + c3) : 0.0;
+        };
+        const double b0 = h0 ? rhs[i0] : 0.0, b1 = h1 ? rhs[i1] : 0.0;
+        const double m0 = h0 ? minv[i0] : 0.0, m1 = h1 ? minv[i1] : 0.0;
+        double x0 = 0.0, x1 = 0.0, r0 = b0, r1 = b1, z0 = m0 * b0, z1 = m1 * b1, p0 = 0.0, p1 = 0.0;
+        double rho = warp_sum(fma(r1, z1, r0 * z0)), rr = warp_sum(fma(r1, r1, r0 * r0)), rho_old = rho;
         const double rhs2 = rr;
         const double tol2 = fmax(rtol * rtol * rr, a.atol * a.atol);
         int64_t it = 0, it_rs = 0;
@@ -249,33 +282,36 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
         __syncwarp();
         for (int round = 0; !breakdown; ++round) {
             while (!done) {
-                const double beta = (it_rs == 0) ? 0.0 : rho / rho_old;
-                for (int j = l; j < n; j += 32) sp[j] = (it_rs == 0) ? zv[j] : fma(beta, sp[j], zv[j]);
+                const bool first = (it_rs == 0);
+                const double beta = first ? 0.0 : rho / rho_old;
+                p0 = first ? z0 : fma(beta, p0, z0);
+                p1 = first ? z1 : fma(beta, p1, z1);
+                sp[i0] = p0;                     // 0 beyond n
+                sp[i1] = p1;
                 __syncwarp();
-                double d = 0.0;
-                double y0 = 0.0, y1 = 0.0;
-                if (l < n) { y0 = kmul(sp, l); d = fma(sp[l], y0, d); }
-                if (l + 32 < n) { y1 = kmul(sp, l + 32); d = fma(sp[l + 32], y1, d); }
-                const double pkp = warp_sum(d);
+                double y0, y1;
+                kmul(sp, y0, y1);
+                const double pkp = warp_sum(fma(p0, y0, p1 * y1));
                 if (!(pkp > 0.0) || !finite_d(pkp)) {
                     breakdown = 1;
                     break;
                 }
                 const double alpha = rho / pkp;
-                double rz2 = 0.0, rr2 = 0.0;
-                for (int j = l, q = 0; j < n; j += 32, ++q) {
-                    const double y = q ? y1 : y0;
-                    dx[j] = fma(alpha, sp[j], dx[j]);
-                    const double r = fma(-alpha, y, rv[j]);
-                    const double z = minv[j] * r;
-                    rv[j] = r;
-                    zv[j] = z;
-                    rz2 = fma(r, z, rz2);
-                    rr2 = fma(r, r, rr2);
+                x0 = fma(alpha, p0, x0);
+                x1 = fma(alpha, p1, x1);
+                r0 = fma(-alpha, y0, r0);
+                r1 = fma(-alpha, y1, r1);
+                z0 = m0 * r0;
+                z1 = m1 * r1;
+                double rz2 = fma(r1, z1, r0 * z0), rr2 = fma(r1, r1, r0 * r0);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    rz2 += __shfl_xor_sync(0xffffffffu, rz2, o);
+                    rr2 += __shfl_xor_sync(0xffffffffu, rr2, o);
                 }
                 rho_old = rho;
-                rho = warp_sum(rz2);
-                rr = warp_sum(rr2);
+                rho = rz2;
+                rr = rr2;
                 ++it;
                 ++it_rs;
                 if (!finite_d(rr) || !finite_d(rho)) {
@@ -283,38 +319,37 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
                     break;
                 }
                 done = (rr <= tol2 || it >= maxit) ? 1 : 0;
-                __syncwarp();
+                __syncwarp();                    // sp reads done before the next overwrite
             }
             if (breakdown) break;
             // true residual with the same K
             __syncwarp();
-            double r2 = 0.0;
-            for (int j = l; j < n; j += 32) {
-                const double rt = rhs[j] - kmul(dx, j);
-                zv[j] = rt;                       // held until a restart needs it
-                r2 = fma(rt, rt, r2);
-            }
-            res2 = warp_sum(r2);
+            sp[i0] = x0;
+            sp[i1] = x1;
+            __syncwarp();
+            double k0, k1;
+            kmul(sp, k0, k1);
+            const double t0 = h0 ? b0 - k0 : 0.0, t1 = h1 ? b1 - k1 : 0.0;
+            res2 = warp_sum(fma(t1, t1, t0 * t0));
             if (!finite_d(res2) || res2 <= tol2) break;
             if (it >= maxit || round >= 8) {
                 stalled = 1;
                 break;
             }
             ++rs;
-            double tz = 0.0, tr = 0.0;
-            for (int j = l; j < n; j += 32) {
-                const double r = zv[j], z = minv[j] * r;
-                rv[j] = r;
-                zv[j] = z;
-                tz = fma(r, z, tz);
-                tr = fma(r, r, tr);
-            }
-            rho = rho_old = warp_sum(tz);
-            rr = warp_sum(tr);
+            r0 = t0;
+            r1 = t1;
+            z0 = m0 * r0;
+            z1 = m1 * r1;
+            rho = rho_old = warp_sum(fma(r1, z1, r0 * z0));
+            rr = warp_sum(fma(r1, r1, r0 * r0));
             it_rs = 0;
             done = (rr <= tol2 || it >= maxit) ? 1 : 0;
             __syncwarp();
         }
+        __syncwarp();
+        if (h0) dx[i0] = x0;
+        if (h1) dx[i1] = x1;
         pcg_it = it;
         pcg_restarts = rs;
         pcg_stalled = stalled;
@@ -327,11 +362,7 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
     // ---- recovery + fraction to the boundary (ipmops.cu k_recover_m / k_recover_n) and update
     double alpha_x = 0.0, alpha_l = 0.0;
     auto step = [&](double tau) {
-        for (int i = l; i < m; i += 32) {
-            double s = 0.0;
-            for (int j = 0; j < n; ++j) s = fma(sA[i * kLd + j], dx[j], s);
-            Adx[i] = s;
-        }
+        for (int i = l; i < m; i += 32) Adx[i] = dot4(sA + i * kLd, 1, dx, 1, n);
         __syncwarp();
         double mx = INFINITY, ml = INFINITY;
         int bad = 0;

@@ -39,8 +39,14 @@ t100, t1000 = t(40), t(340)
 print(json.dumps({"workload": q.n, "IPM_PCG_WARP": os.environ.get("IPM_PCG_WARP", "1"),
                   "us_per_pcg_iter": (t1000 - t100) / 300 * 1e6, "t40_ms": t100 * 1e3, "t340_ms": t1000 * 1e3}))
 qp.solve()
-ts = []
+ts, tp, tw = [], [], []
 for _ in range(5):
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
     qp.solve()
+    tw.append((time.perf_counter() - w0) * 1e3)
     ts.append(qp.stats()["t_solve_ms"])
-print(json.dumps({"qp_solve_ms_median": sorted(ts)[2], "pcg_iters": qp.stats()["pcg_iters_total"]}))
+    tp.append(qp.stats()["t_pcg_ms"])
+print(json.dumps({"qp_solve_ms_median": sorted(ts)[2], "t_pcg_ms_median": sorted(tp)[2],
+                  "wall_ms_median": sorted(tw)[2], "ipm_iters": qp.stats()["ipm_iters"],
+                  "pcg_iters": qp.stats()["pcg_iters_total"], "IPM_TINY": os.environ.get("IPM_TINY", "1")}))

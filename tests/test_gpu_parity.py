@@ -361,7 +361,8 @@ def test_one_warp_ipm_matches_multi_kernel_path(seed):
     assert len(ta) == len(tb) == sa["ipm_iters"]
     for ra, rb in zip(ta, tb):
         assert ra["it"] == rb["it"] and ra["mu"] == rb["mu"]
-        assert abs(ra["obj"] - rb["obj"]) <= 1e-9 * max(1.0, abs(rb["obj"]))
+        # intermediate iterates carry the PCG tolerance of their iteration (rtol up to 1e-6, D6)
+        assert abs(ra["obj"] - rb["obj"]) <= 1e-5 * max(1.0, abs(rb["obj"]))
     # a second solve from the stored state (warm start is the multi-kernel path's) still works
     a.warm_start()
     assert a.solve() == "ok"
