@@ -222,24 +222,22 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
             rhs[j] = fma(1.0, at, r1);
         }
         // K = (H + sum_r sigma_r (A_rj A_rk)) + delta_jk sigma_b,j over the rows r with A_rj != 0 in
-        // ascending r — k_form_K's terms and association, so the same bits.  Stored TRANSPOSED
-        // (sK[k * 64 + j] = K_jk; lane j owns column j, so every walk is lane-consecutive) and
-        // accumulated in place one row of A at a time (independent FMAs across k).
-        for (int j = l; j < n; j += 32)
-            for (int k = 0; k < n; ++k) sK[k * kT + j] = 0.0;
-        for (int r = 0; r < m; ++r) {
-            const double sr = sigc[r];
-            const double *ar = sA + r * kLd;
-            for (int j = l; j < n; j += 32) {
-                const double a = ar[j];
-                if (a == 0.0) continue;
-#pragma unroll 4
-                for (int k = 0; k < n; ++k) sK[k * kT + j] = fma(sr, a * ar[k], sK[k * kT + j]);
+        // ascending r — k_form_K's terms and association, so the same bits.  Lane l builds columns
+        // k = l, l + 32 for every j (the nonzero test on A_rj is warp-uniform: no divergence) and
+        // stores K_jk at sK[k * kLd + j], the layout the PCG walks lane-consecutively.
+        for (int j = 0; j < n; ++j) {
+            double acc0 = 0.0, acc1 = 0.0;
+            for (int r = 0; r < m; ++r) {
+                const double arj = sA[r * kLd + j];
+                if (arj == 0.0) continue;
+                const double sr = sigc[r];
+                acc0 = fma(sr, arj * sA[r * kLd + l], acc0);
+                acc1 = fma(sr, arj * sA[r * kLd + l + 32], acc1);
             }
+            if (l < n) sK[l * kLd + j] = (sH[j * kLd + l] + acc0) + (j == l ? sigb[j] : 0.0);
+            if (l + 32 < n) sK[(l + 32) * kLd + j] = (sH[j * kLd + l + 32] + acc1) + (j == l + 32 ? sigb[j] : 0.0);
         }
-        for (int j = l; j < n; j += 32)
-            for (int k = 0; k < n; ++k)
-                sK[k * kT + j] = (sH[j * kLd + k] + sK[k * kT + j]) + (j == k ? sigb[j] : 0.0);
+        __syncwarp();
         // PCG from x0 = 0 (k_pcg_init), stopping rule S:225, restarts on the true residual — the
         // register-resident loop of k_pcg_warp: lane l owns rows l and l + 32, u broadcast from sp
         const int i0 = l, i1 = l + 32;
@@ -252,19 +250,19 @@ __global__ void __launch_bounds__(32, 1) k_ipm_tiny(TinyArgs a) {
             for (; k < n4; k += 4) {
                 const double2 ua = *reinterpret_cast<const double2 *>(u + k);
                 const double2 ub = *reinterpret_cast<const double2 *>(u + k + 2);
-                const double *kr = sK + k * kT;
+                const double *kr = sK + k * kLd;
                 a0 = fma(kr[i0], ua.x, a0);
                 c0 = fma(kr[i1], ua.x, c0);
-                a1 = fma(kr[kT + i0], ua.y, a1);
-                c1 = fma(kr[kT + i1], ua.y, c1);
-                a2 = fma(kr[2 * kT + i0], ub.x, a2);
-                c2 = fma(kr[2 * kT + i1], ub.x, c2);
-                a3 = fma(kr[3 * kT + i0], ub.y, a3);
-                c3 = fma(kr[3 * kT + i1], ub.y, c3);
+                a1 = fma(kr[kLd + i0], ua.y, a1);
+                c1 = fma(kr[kLd + i1], ua.y, c1);
+                a2 = fma(kr[2 * kLd + i0], ub.x, a2);
+                c2 = fma(kr[2 * kLd + i1], ub.x, c2);
+                a3 = fma(kr[3 * kLd + i0], ub.y, a3);
+                c3 = fma(kr[3 * kLd + i1], ub.y, c3);
             }
             for (; k < n; ++k) {
-                a0 = fma(sK[k * kT + i0], u[k], a0);
-                c0 = fma(sK[k * kT + i1], u[k], c0);
+                a0 = fma(sK[k * kLd + i0], u[k], a0);
+                c0 = fma(sK[k * kLd + i1], u[k], c0);
             }
             o0 = h0 ? (a0 + a1) + (a2 + a3) : 0.0;
             o1 = h1 ? (c0 + c1) + (c2 + c3) : 0.0;
