@@ -2,7 +2,8 @@
 k_pcg_small), a 3000-variable VMAT-shaped QP (SYMV mbarrier ring + named barrier, SpMV side
 branch, cooperative fused update with its grid barrier, graph WHILE loop), and optionally the
 same QP row-sharded over 2 in-process ranks (peer data plane).
-  compute-sanitizer --tool racecheck python scripts/sanitize_run.py [--case solve|opapply|pcgiter|sharded]"""
+  compute-sanitizer --tool racecheck python scripts/sanitize_run.py [--case solve|c1|c1pcg|opapply|pcgiter|sharded]
+(C1 solves now run the whole IPM loop in one warp, k_ipm_tiny; c1pcg = the one-warp PCG hooks)"""
 import argparse
 import os
 import sys
@@ -37,6 +38,13 @@ elif a.case in ("opapply", "pcgiter"):
         print("opapply", float(qp.op_apply(sb, sc, v).sum()), flush=True)
     else:
         print("pcgiter", qp.pcg_iterate(sb, sc, v, 3)["rho"], flush=True)
+elif a.case == "c1pcg":                            # one-warp PCG on the assembled K (k_form_K + k_pcg_warp)
+    q = config("C1", 0)
+    qp = QP(device=dev, **problem_tensors(q, dev))
+    sb, sc, v = rng.uniform(0, 3, q.n), 10.0 ** rng.uniform(-2, 2, q.m), rng.normal(size=q.n)
+    print("c1pcg", qp.pcg_iterate(sb, sc, v, 5)["rho"], flush=True)
+    x, it = qp.pcg(sb, sc, v, 1e-10)
+    print("c1pcg solve", it, flush=True)
 elif a.case == "sharded":
     from paper_2405_03584_b200.dist import LocalGroup, partition
     q = planted_qp(1000, 300, density=0.02, rank=32, seed=43, rows="vmat", var="box")
